@@ -1,0 +1,128 @@
+/*
+ * flowtree.h — C ABI of the B200-native Flowtree query path (arXiv 1910.04126).
+ *
+ * Problem (§1): X ⊂ R^d is a finite ground set, μ_1..μ_n are distributions on X
+ * with support ≤ s, and ν is a query distribution; find the k μ_i closest to ν in W1 (Eq. (1),
+ * PAPER.md:21-26).  The library estimates W1(ν, μ_i) with
+ *   - the Quadtree estimate   Σ_v 2^{ℓ(v)} |μ(v) − ν(v)|            (§2), and
+ *   - the Flowtree estimate   Σ f(x,x') ||x − x'||, f = tree-optimal flow  (§3;
+ *                              greedy bottom-up computation, App. A.1),
+ * and ranks with the prefetch-and-prune pipeline Quadtree → top-m → Flowtree → top-k
+ * (§4.4).  The readings of the paper that fix every unstated detail
+ * (cell rule, node numbering, tie-break, integer masses) are DESIGN.md §3 R1-R18.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns ft_status; FT_OK = 0.  On failure ft_last_error() returns a
+ *     thread-local message naming the argument or record at fault.  Nothing is written to the
+ *     outputs of a call that fails on the host.
+ *   - Distributions are CSR: offsets (int64, n+1, offsets[0] = 0), vocab ids (int32, in
+ *     [0, N)) and integer masses (uint32 ≥ 1).  A distribution must be non-empty, have no
+ *     duplicate id, and total mass ≤ 65535 (so W·U < 2^32, R13): FT_EINVAL /
+ *     FT_ERANGE / FT_EOVERFLOW otherwise.  Estimates are in normalised W1 units (masses summing
+ *     to 1), as doubles.
+ *   - Build/load inputs are host arrays, copied; the caller keeps ownership.  Index and dataset
+ *     are opaque, library-owned and device resident (current CUDA device at creation).  Free a
+ *     dataset before its index.  Neither is safe for concurrent calls from several threads.
+ *   - Query calls: q_off is a HOST array (the batch shape).  q_ids, q_w, docs and every output
+ *     may be host or device pointers (detected with cudaPointerGetAttributes).  If every output
+ *     is a device pointer the call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and device-side validation errors of the query payload are reported by
+ *     the next ft_synchronize() (sticky); otherwise the call synchronises `stream` before
+ *     returning and reports them itself.  Scratch is cached per dataset: no device allocation
+ *     after the first call at a given size.
+ *   - Limits: support ≤ 2048 per distribution; support × tree depth ≤ 8192; k and prefilter_m
+ *     ≤ 8192; N < 2^30; nnz < 2^32.
+ */
+#ifndef FLOWTREE_H
+#define FLOWTREE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FT_OK = 0,
+    FT_EINVAL = 1,     /* invalid argument / record (empty, zero mass, duplicate id, bad k) */
+    FT_ERANGE = 2,     /* vocab id outside [0, N), or a size limit exceeded */
+    FT_EOVERFLOW = 3,  /* total mass > 65535, or a Quadtree numerator ≥ 2^53 */
+    FT_ENOMEM = 4,     /* device or host allocation failed */
+    FT_ECUDA = 5,      /* CUDA runtime error */
+    FT_ESTATE = 6      /* object in an unusable state (e.g. NULL handle) */
+} ft_status;
+
+typedef struct ft_index ft_index;
+typedef struct ft_dataset ft_dataset;
+
+/* Build the randomly shifted quadtree over X (§2 "Generic Quadtree").
+ *   X          host float32 [N × d], row-major; copied to the device.
+ *   seed       σ_i = Φ · (SplitMix64(seed, i) >> 11) · 2^-53 (R3).
+ *   max_depth  depth cap D (number of halvings), ≤ 0 → 32, must be ≤ 52 (R5).
+ * Node ids are breadth first, children ordered by (parent id, child bit-vector, dim 0 first)
+ * (R7); cells are half-open (R4); the cell rule is evaluated in FP64 exactly as the
+ * oracle does, so the node ids match it bit for bit.  FT_EINVAL if N < 1, d < 1 or D > 52.   */
+ft_status ft_build_quadtree(const float* X, int64_t N, int32_t d, uint64_t seed, int32_t max_depth,
+                            ft_index** out);
+/* Same with an explicit shift σ (host double [d], each in [0, Φ]) — test hook.               */
+ft_status ft_build_quadtree_shift(const float* X, int64_t N, int32_t d, const double* sigma,
+                                  int32_t max_depth, ft_index** out);
+/* Φ (max coordinate range), ℓ_root = ⌈log2 Φ⌉+1, realised depth D*, number of nodes.  Any
+ * output pointer may be NULL.                                                                */
+ft_status ft_index_info(const ft_index* ix, double* phi, int32_t* l_root, int32_t* d_star, int64_t* n_nodes);
+/* Parity hook: host int32 [N × (D*+1)], node id of point x at depth k, −1 below its leaf.      */
+ft_status ft_index_paths(const ft_index* ix, int32_t* out);
+/* Parity hook: host double [d], the shift σ actually used.                                    */
+ft_status ft_index_sigma(const ft_index* ix, double* sigma);
+/* Parity hook: host int32 [M] node depths and [M] ground-point counts (either may be NULL).   */
+ft_status ft_index_nodes(const ft_index* ix, int32_t* depth, int32_t* count);
+
+/* Load n documents (host CSR, copied) into the node-sorted device layout:
+ * a vocab-sorted Flowtree record, the M-node lists, and the node-sorted Quadtree record
+ * (the ℓ1 embedding of PAPER.md:131-134).  Errors name the first offending document.         */
+ft_status ft_load_dataset(const ft_index* ix, const int64_t* doc_off, int64_t n, const int32_t* ids,
+                          const uint32_t* w, ft_dataset** out);
+/* n, nnz, number of Quadtree node records, max support.  Any pointer may be NULL.            */
+ft_status ft_dataset_info(const ft_dataset* ds, int64_t* n, int64_t* nnz, int64_t* n_qt_records,
+                          int32_t* max_support);
+
+/* Quadtree estimates for every (query, doc) pair.
+ *   q_off   HOST int64 [nq+1];  q_ids int32 / q_w uint32 [q_off[nq]] (host or device).
+ *   docs    int64 [n_docs] doc indices, or NULL for all n docs (then n_docs is ignored).
+ *   out     double [nq × n_docs] row-major (host or device).
+ * Values are bit-identical to the oracle (exact integer numerator, two correctly rounded ops). */
+ft_status ft_quadtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                               const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
+                               void* stream);
+/* Flowtree estimates with the same signature.  The flow is integer exact;
+ * distances are FP32 (|rel err| ≲ 1e-6), accumulation FP64; tolerance 1e-5 relative.        */
+ft_status ft_flowtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                               const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
+                               void* stream);
+/* Parity hook: the Flowtree flow of one (query, doc) pair, HOST outputs, in canonical order
+ * (node depth desc, node id asc, src asc, dst asc) — the oracle's emission order.
+ *   src = doc vocab id, dst = query vocab id, mass in units of 1/(W·U), node where matched.
+ *   FT_ERANGE if more than cap triples (n_out still receives the count).                     */
+ft_status ft_flowtree_flow(const ft_dataset* ds, int32_t q_len, const int32_t* q_ids, const uint32_t* q_w,
+                           int64_t doc, int32_t* src, int32_t* dst, uint64_t* mass, int32_t* node, int32_t cap,
+                           int32_t* n_out);
+/* k-NN: for each query the k docs with the smallest Flowtree estimate, ties by
+ * doc id.  prefilter_m == 0 or ≥ n: exhaustive Flowtree; else Quadtree over all docs, keep
+ * the m smallest (value, id), Flowtree on those, keep k.  FT_EINVAL if
+ * k < 1 or 0 < prefilter_m < k.  If fewer than k candidates, pads with id −1 / value +inf.
+ *   out_ids int64 [nq × k], out_val double [nq × k] (host or device).                        */
+ft_status ft_knn(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                 const uint32_t* q_w, int32_t k, int64_t prefilter_m, int64_t* out_ids, double* out_val,
+                 void* stream);
+/* Synchronise `stream` and report (then clear) any sticky device-side validation error.      */
+ft_status ft_synchronize(const ft_dataset* ds, void* stream);
+
+void ft_index_free(ft_index* ix);
+void ft_dataset_free(ft_dataset* ds);
+/* Thread-local message of the last failing call on this thread ("" if none).                 */
+const char* ft_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWTREE_H */

@@ -1,0 +1,353 @@
+// ft_api.cu — the C ABI query entry points (include/flowtree.h): argument validation, host/device
+// pointer handling, scratch management and the stage sequence of the hot path
+//   a2 query prep → a3 Quadtree → a4 top-m → a5 distance table → a6 Flowtree → a7 top-k.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ft_device.cuh"
+
+static thread_local std::string g_last_error;
+
+ft_status fti_fail(ft_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+extern "C" const char* ft_last_error(void) { return g_last_error.c_str(); }
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+#define FTI_RES(buf, bytes)                                                                     \
+    do {                                                                                        \
+        cudaError_t _e = (buf).reserve(bytes);                                                  \
+        if (_e != cudaSuccess) return fti_fail(FT_ENOMEM, std::string("scratch allocation: ") + \
+                                                              cudaGetErrorString(_e));          \
+    } while (0)
+
+// device error word (sticky) -> status
+ft_status check_device_errors(const ft_dataset* ds, cudaStream_t st, const char* who) {
+    uint32_t h = 0;
+    FTI_CUDA(cudaMemcpyAsync(&h, ds->err_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    FTI_CUDA(cudaStreamSynchronize(st));
+    if (h == 0) return FT_OK;
+    FTI_CUDA(cudaMemsetAsync(ds->err_dev, 0, sizeof(uint32_t), st));
+    FTI_CUDA(cudaStreamSynchronize(st));
+    std::string w = std::string(who) + ": device-side validation failed: ";
+    if (h & FTI_ERR_RANGE) return fti_fail(FT_ERANGE, w + "vocab or doc id out of range");
+    if (h & FTI_ERR_OVERFLOW) return fti_fail(FT_EOVERFLOW, w + "total mass > 65535 or Quadtree numerator >= 2^53");
+    return fti_fail(FT_EINVAL, w + "empty query, zero mass or duplicate vocab id");
+}
+
+struct Staged {
+    QueryLayout L;
+    const int32_t* qids = nullptr;
+    const uint32_t* qw = nullptr;
+    const int64_t* qoff_dev = nullptr;
+    uint8_t* qblock = nullptr;
+};
+
+// validate the batch shape (host q_off) and, for host payloads, the payload itself; stage to the
+// device; run the a2 prep kernel.
+ft_status stage_queries(ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids, const uint32_t* q_w,
+                        cudaStream_t st, const char* who, Staged& S) {
+    const ft_index* ix = ds->ix;
+    if (!q_off || !q_ids || !q_w) return fti_fail(FT_EINVAL, std::string(who) + ": NULL query array");
+    if (nq < 1) return fti_fail(FT_EINVAL, std::string(who) + ": need nq >= 1");
+    if (is_device_ptr(q_off)) return fti_fail(FT_EINVAL, std::string(who) + ": q_off must be a host array");
+    if (q_off[0] != 0) return fti_fail(FT_EINVAL, std::string(who) + ": q_off[0] must be 0");
+    int32_t smax = 0;
+    for (int32_t q = 0; q < nq; q++) {
+        int64_t s = q_off[q + 1] - q_off[q];
+        if (s < 1) return fti_fail(FT_EINVAL, std::string(who) + ": query " + std::to_string(q) + " is empty");
+        if (s > FTI_MAX_SUPPORT)
+            return fti_fail(FT_ERANGE, std::string(who) + ": query " + std::to_string(q) + " has support > 2048");
+        smax = std::max<int32_t>(smax, (int32_t)s);
+    }
+    if ((int64_t)smax * std::max(1, ix->d_star) > FTI_MAX_NODE_ENTRIES)
+        return fti_fail(FT_ERANGE, std::string(who) + ": query support x tree depth exceeds 8192 entries");
+    const int64_t nnz = q_off[nq];
+    const bool dev_ids = is_device_ptr(q_ids), dev_w = is_device_ptr(q_w);
+    if (!dev_ids && !dev_w) {
+        // full host validation with precise messages
+        std::vector<int32_t> tmp;
+        for (int32_t q = 0; q < nq; q++) {
+            uint64_t U = 0;
+            tmp.assign(q_ids + q_off[q], q_ids + q_off[q + 1]);
+            for (int64_t t = q_off[q]; t < q_off[q + 1]; t++) {
+                if (q_ids[t] < 0 || (int64_t)q_ids[t] >= ix->N)
+                    return fti_fail(FT_ERANGE, std::string(who) + ": query " + std::to_string(q) + ": vocab id " +
+                                                   std::to_string(q_ids[t]) + " outside [0, N)");
+                if (q_w[t] == 0)
+                    return fti_fail(FT_EINVAL, std::string(who) + ": query " + std::to_string(q) + ": zero mass");
+                U += q_w[t];
+            }
+            if (U > FTI_MAX_WEIGHT_TOTAL)
+                return fti_fail(FT_EOVERFLOW, std::string(who) + ": query " + std::to_string(q) + ": total mass > 65535");
+            std::sort(tmp.begin(), tmp.end());
+            if (std::adjacent_find(tmp.begin(), tmp.end()) != tmp.end())
+                return fti_fail(FT_EINVAL, std::string(who) + ": query " + std::to_string(q) + ": duplicate vocab id");
+        }
+    }
+    S.L = fti_query_layout(ix, smax);
+    FTI_RES(ds->s_qoff, sizeof(int64_t) * (nq + 1));
+    FTI_CUDA(cudaMemcpyAsync(ds->s_qoff.p, q_off, sizeof(int64_t) * (nq + 1), cudaMemcpyHostToDevice, st));
+    S.qoff_dev = ds->s_qoff.as<int64_t>();
+    if (dev_ids) S.qids = q_ids;
+    else {
+        FTI_RES(ds->s_qids, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+        FTI_CUDA(cudaMemcpyAsync(ds->s_qids.p, q_ids, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+        S.qids = ds->s_qids.as<int32_t>();
+    }
+    if (dev_w) S.qw = q_w;
+    else {
+        FTI_RES(ds->s_qw, sizeof(uint32_t) * std::max<int64_t>(nnz, 1));
+        FTI_CUDA(cudaMemcpyAsync(ds->s_qw.p, q_w, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st));
+        S.qw = ds->s_qw.as<uint32_t>();
+    }
+    FTI_RES(ds->s_qblock, S.L.stride * (size_t)nq);
+    S.qblock = ds->s_qblock.as<uint8_t>();
+    FTI_CUDA(fti_launch_query_prep(ix, S.L, S.qoff_dev, nq, S.qids, S.qw, S.qblock, ds->err_dev, st));
+    return FT_OK;
+}
+
+// docs argument: NULL = all; host arrays are validated and copied; device arrays are checked in-kernel.
+ft_status stage_docs(ft_dataset* ds, const int64_t* docs, int64_t n_docs, cudaStream_t st, const char* who,
+                     const int64_t** out, int64_t* n_out) {
+    if (!docs) {
+        *out = nullptr;
+        *n_out = ds->n;
+        return FT_OK;
+    }
+    if (n_docs < 1) return fti_fail(FT_EINVAL, std::string(who) + ": need n_docs >= 1");
+    if (is_device_ptr(docs)) {
+        *out = docs;
+        *n_out = n_docs;
+        return FT_OK;
+    }
+    for (int64_t i = 0; i < n_docs; i++)
+        if (docs[i] < 0 || docs[i] >= ds->n)
+            return fti_fail(FT_ERANGE, std::string(who) + ": docs[" + std::to_string(i) + "] outside [0, n)");
+    FTI_RES(ds->s_docs, sizeof(int64_t) * n_docs);
+    FTI_CUDA(cudaMemcpyAsync(ds->s_docs.p, docs, sizeof(int64_t) * n_docs, cudaMemcpyHostToDevice, st));
+    *out = ds->s_docs.as<int64_t>();
+    *n_out = n_docs;
+    return FT_OK;
+}
+
+// a5 + a6 over a query batch, chunked so the distance tables stay within a memory budget.
+ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int64_t* d_docs, int64_t docs_ld,
+                         int64_t n_docs, double* d_out, int64_t out_ld, cudaStream_t st) {
+    const ft_index* ix = ds->ix;
+    if (ix->d <= FTI_SMALL_D) {
+        FTI_CUDA(fti_launch_ft(ds, S.L, S.qblock, nq, d_docs, docs_ld, n_docs, FtTable{}, d_out, out_ld, nullptr,
+                               nullptr, 0, st));
+        return FT_OK;
+    }
+    const int32_t ld = (S.L.smax + 3) & ~3;
+    const bool use_map = d_docs != nullptr;
+    const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
+    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? (size_t)ix->N * 4 + (size_t)rows_cap * 4 + 4 : 0);
+    const size_t budget = (size_t)3 << 30;
+    int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
+    FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
+    if (use_map) {
+        FTI_RES(ds->s_map, (size_t)qch * ix->N * 4);
+        FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);
+        FTI_RES(ds->s_rowcnt, (size_t)qch * 4);
+    }
+    for (int32_t q0 = 0; q0 < nq; q0 += qch) {
+        const int32_t nqc = std::min(qch, nq - q0);
+        const uint8_t* qb = S.qblock + (size_t)q0 * S.L.stride;
+        const int64_t* dq = d_docs ? d_docs + (int64_t)q0 * docs_ld : nullptr;
+        FtTable tab;
+        tab.table = ds->s_table.as<float>();
+        tab.rows_cap = rows_cap;
+        tab.ld = ld;
+        if (use_map) {
+            FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<int32_t>(),
+                                          ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap, st));
+            tab.map = ds->s_map.as<int32_t>();
+        }
+        FTI_CUDA(fti_launch_dist_table(ix, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
+                                       use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
+                                       ds->s_table.as<float>(), ld, st));
+        FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,
+                               nullptr, nullptr, 0, st));
+    }
+    return FT_OK;
+}
+
+ft_status estimate_common(const ft_dataset* cds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                          const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out, void* stream,
+                          bool flowtree, const char* who) {
+    if (!cds) return fti_fail(FT_ESTATE, std::string(who) + ": NULL dataset");
+    if (!out) return fti_fail(FT_EINVAL, std::string(who) + ": out is NULL");
+    ft_dataset* ds = const_cast<ft_dataset*>(cds);
+    cudaStream_t st = (cudaStream_t)stream;
+    Staged S;
+    ft_status rc = stage_queries(ds, q_off, nq, q_ids, q_w, st, who, S);
+    if (rc) return rc;
+    const int64_t* d_docs;
+    int64_t nd;
+    rc = stage_docs(ds, docs, n_docs, st, who, &d_docs, &nd);
+    if (rc) return rc;
+    const bool dev_out = is_device_ptr(out);
+    double* d_out = out;
+    if (!dev_out) {
+        FTI_RES(ds->s_vals, sizeof(double) * nq * nd);
+        d_out = ds->s_vals.as<double>();
+    }
+    if (flowtree) {
+        rc = flowtree_stage(ds, S, nq, d_docs, 0, nd, d_out, nd, st);
+        if (rc) return rc;
+    } else {
+        FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, d_docs, 0, nd, d_out, nd, st));
+    }
+    if (!dev_out) {
+        FTI_CUDA(cudaMemcpyAsync(out, d_out, sizeof(double) * nq * nd, cudaMemcpyDeviceToHost, st));
+        return check_device_errors(ds, st, who);
+    }
+    return FT_OK;
+}
+
+}  // namespace
+
+extern "C" ft_status ft_quadtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                                          const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
+                                          void* stream) {
+    return estimate_common(ds, q_off, nq, q_ids, q_w, docs, n_docs, out, stream, false, "ft_quadtree_estimate");
+}
+
+extern "C" ft_status ft_flowtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                                          const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
+                                          void* stream) {
+    return estimate_common(ds, q_off, nq, q_ids, q_w, docs, n_docs, out, stream, true, "ft_flowtree_estimate");
+}
+
+extern "C" ft_status ft_flowtree_flow(const ft_dataset* cds, int32_t q_len, const int32_t* q_ids, const uint32_t* q_w,
+                                      int64_t doc, int32_t* src, int32_t* dst, uint64_t* mass, int32_t* node,
+                                      int32_t cap, int32_t* n_out) {
+    const char* who = "ft_flowtree_flow";
+    if (!cds) return fti_fail(FT_ESTATE, "ft_flowtree_flow: NULL dataset");
+    ft_dataset* ds = const_cast<ft_dataset*>(cds);
+    if (doc < 0 || doc >= ds->n) return fti_fail(FT_ERANGE, "ft_flowtree_flow: doc outside [0, n)");
+    if (cap < 0 || !n_out) return fti_fail(FT_EINVAL, "ft_flowtree_flow: bad cap / n_out");
+    cudaStream_t st = 0;
+    int64_t q_off[2] = {0, q_len};
+    Staged S;
+    ft_status rc = stage_queries(ds, q_off, 1, q_ids, q_w, st, who, S);
+    if (rc) return rc;
+    int64_t ndoc = doc;
+    FTI_RES(ds->s_docs, sizeof(int64_t));
+    FTI_CUDA(cudaMemcpyAsync(ds->s_docs.p, &ndoc, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    const int32_t fcap = ds->max_s + q_len + 8;
+    FTI_RES(ds->s_flow, sizeof(uint32_t) * 4 * fcap);
+    FTI_RES(ds->s_flowcnt, sizeof(uint32_t));
+    FTI_CUDA(cudaMemsetAsync(ds->s_flowcnt.p, 0, sizeof(uint32_t), st));
+    FTI_RES(ds->s_vals, sizeof(double));
+    FTI_CUDA(fti_launch_ft(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{}, ds->s_vals.as<double>(), 1,
+                           ds->s_flow.as<uint32_t>(), ds->s_flowcnt.as<uint32_t>(), fcap, st));
+    uint32_t cnt = 0;
+    FTI_CUDA(cudaMemcpyAsync(&cnt, ds->s_flowcnt.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    rc = check_device_errors(ds, st, who);
+    if (rc) return rc;
+    const uint32_t nget = std::min<uint32_t>(cnt, (uint32_t)fcap);
+    std::vector<uint32_t> f(4 * (size_t)nget);
+    FTI_CUDA(cudaMemcpy(f.data(), ds->s_flow.p, sizeof(uint32_t) * 4 * nget, cudaMemcpyDeviceToHost));
+    // canonical order (depth desc, node asc, src asc, dst asc) = the oracle's emission order
+    const ft_index* ix = ds->ix;
+    auto depth_of = [&](uint32_t v) {
+        int k = (int)(std::upper_bound(ix->level_base.begin(), ix->level_base.end(), (int64_t)v) -
+                      ix->level_base.begin()) - 1;
+        return k;
+    };
+    std::vector<uint32_t> ord(nget);
+    for (uint32_t i = 0; i < nget; i++) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
+        int da = depth_of(f[4 * a + 3]), db = depth_of(f[4 * b + 3]);
+        if (da != db) return da > db;
+        for (int t : {3, 0, 1})
+            if (f[4 * a + t] != f[4 * b + t]) return f[4 * a + t] < f[4 * b + t];
+        return false;
+    });
+    *n_out = (int32_t)cnt;
+    if ((int32_t)cnt > cap) return fti_fail(FT_ERANGE, "ft_flowtree_flow: more triples than cap");
+    for (uint32_t i = 0; i < nget; i++) {
+        const uint32_t* t = &f[4 * ord[i]];
+        if (src) src[i] = (int32_t)t[0];
+        if (dst) dst[i] = (int32_t)t[1];
+        if (mass) mass[i] = t[2];
+        if (node) node[i] = (int32_t)t[3];
+    }
+    return FT_OK;
+}
+
+extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                            const uint32_t* q_w, int32_t k, int64_t prefilter_m, int64_t* out_ids, double* out_val,
+                            void* stream) {
+    const char* who = "ft_knn";
+    if (!cds) return fti_fail(FT_ESTATE, "ft_knn: NULL dataset");
+    if (!out_ids || !out_val) return fti_fail(FT_EINVAL, "ft_knn: NULL output");
+    if (k < 1) return fti_fail(FT_EINVAL, "ft_knn: need k >= 1");
+    if (prefilter_m > 0 && prefilter_m < k) return fti_fail(FT_EINVAL, "ft_knn: need prefilter_m == 0 or >= k");
+    if (k > FTI_MAX_SELECT) return fti_fail(FT_ERANGE, "ft_knn: k > 8192");
+    ft_dataset* ds = const_cast<ft_dataset*>(cds);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool exhaustive = prefilter_m <= 0 || prefilter_m >= ds->n;
+    if (!exhaustive && prefilter_m > FTI_MAX_SELECT) return fti_fail(FT_ERANGE, "ft_knn: prefilter_m > 8192");
+    Staged S;
+    ft_status rc = stage_queries(ds, q_off, nq, q_ids, q_w, st, who, S);
+    if (rc) return rc;
+    const bool dev_out = is_device_ptr(out_ids) && is_device_ptr(out_val);
+    int64_t* d_ids = out_ids;
+    double* d_val = out_val;
+    if (!dev_out) {
+        FTI_RES(ds->s_outid, sizeof(int64_t) * nq * k);
+        FTI_RES(ds->s_outval, sizeof(double) * nq * k);
+        d_ids = ds->s_outid.as<int64_t>();
+        d_val = ds->s_outval.as<double>();
+    }
+    const int64_t n = ds->n;
+    if (exhaustive) {
+        FTI_RES(ds->s_vals, sizeof(double) * nq * n);
+        rc = flowtree_stage(ds, S, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st);
+        if (rc) return rc;
+        FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, k, d_ids, d_val, k, st));
+    } else {
+        const int64_t m = prefilter_m;
+        FTI_RES(ds->s_vals, sizeof(double) * nq * n);
+        FTI_RES(ds->s_cand, sizeof(int64_t) * nq * m);
+        FTI_RES(ds->s_vals2, sizeof(double) * nq * m);
+        FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st));
+        FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m, ds->s_cand.as<int64_t>(),
+                                   ds->s_vals2.as<double>(), m, st));
+        rc = flowtree_stage(ds, S, nq, ds->s_cand.as<int64_t>(), m, m, ds->s_vals2.as<double>(), m, st);
+        if (rc) return rc;
+        FTI_CUDA(fti_launch_select(ds->s_vals2.as<double>(), m, ds->s_cand.as<int64_t>(), m, m, nq, k, d_ids, d_val,
+                                   k, st));
+    }
+    if (!dev_out) {
+        FTI_CUDA(cudaMemcpyAsync(out_ids, d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));
+        FTI_CUDA(cudaMemcpyAsync(out_val, d_val, sizeof(double) * nq * k, cudaMemcpyDeviceToHost, st));
+        return check_device_errors(ds, st, who);
+    }
+    return FT_OK;
+}
+
+extern "C" ft_status ft_synchronize(const ft_dataset* ds, void* stream) {
+    if (!ds) return fti_fail(FT_ESTATE, "ft_synchronize: NULL dataset");
+    return check_device_errors(ds, (cudaStream_t)stream, "ft_synchronize");
+}

@@ -1,0 +1,335 @@
+// ft_flow.cu — a6: Flowtree estimate kernel (§3; greedy flow PAPER.md:495-504).
+//
+// One warp per (query, doc) pair.  Masses are cross-scaled integers (reading R13): μ'(x) = w_x·U,
+// ν'(y) = u_y·W, both totalling W·U < 2^32, so every residual and prefix sum is an exact u32.
+// The greedy bottom-up flow with the canonical tie-break (reading R10: at every node, residual
+// lists in ascending vocab id, two-pointer northwest corner) is evaluated in three phases that
+// visit exactly the nodes where matching can happen (C_μ(v), C_ν(v) ≠ ∅):
+//   A  singleton leaves: a vocab id present on both sides self-matches min(μ', ν') at its leaf
+//      (reading R8), distance 0;
+//   B  M-nodes (cells holding ≥ 2 ground points) present on both sides, deepest first, each a
+//      northwest corner over the vocab-ordered residual lists under it;
+//   C  the root: northwest corner over all residuals in vocab order.
+// Each northwest corner is computed in parallel: inclusive prefix sums S of both residual lists
+// (warp scans), T = min of the totals, and every μ-item emits its overlaps with the ν-items
+// whose cumulative intervals meet [S_{i−1}, min(S_i, T)) — the same set of triples the
+// sequential two-pointer produces.  Leftovers: r_i ← max(0, S_i − max(S_{i−1}, T)).
+// The flow is priced with FP32 Euclidean distances (on the fly for d ≤ 32, else from the a5
+// table) and accumulated in FP64: FT = Σ η·dist / (W·U).
+#include <algorithm>
+
+#include "ft_device.cuh"
+
+namespace {
+
+struct FtArgs {
+    const uint32_t* doc_off;
+    const uint2* items;
+    const uint32_t* Wd;
+    const uint32_t* mn_off;
+    const uint4* mnodes;
+    const uint16_t* mlists;
+    const float* X;
+    int d;
+    const int32_t* path;
+    int cols;
+    const uint8_t* leaf_depth;
+    int64_t N;
+    const uint8_t* qblock;
+    QueryLayout L;
+    int32_t nq;
+    const int64_t* docs;
+    int64_t docs_ld;
+    int64_t n_docs;
+    int64_t docs_per_cta;
+    FtTable tab;
+    double* out;
+    int64_t out_ld;
+    uint32_t* flow;
+    uint32_t* flowcnt;
+    int flow_cap;
+    int Sd, Sq;
+    int small_d;
+    int64_t n;
+    uint32_t* err;
+};
+
+constexpr int FT_WARPS = 8;
+
+struct PairCtx {
+    const FtArgs* a;
+    int q;
+    const uint2* qitem;     // smem
+    const float* Y;         // smem (small d) or null
+    uint32_t* dvoc;         // per-warp smem
+    uint32_t* dres;
+    uint32_t* dcum;
+    uint32_t* qres;
+    uint32_t* qcum;
+    const float* trow_base; // table for this query or null
+    const int32_t* map;     // vocab -> row map for this query or null
+};
+
+__device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_t y, int jq) {
+    const FtArgs& a = *c.a;
+    if (c.trow_base) {
+        int64_t row = c.map ? (int64_t)c.map[x] : (int64_t)x;
+        return c.trow_base[row * a.tab.ld + jq];
+    }
+    // on the fly, FP32 direct differences (the query row from shared memory when staged)
+    const float* xr = a.X + (int64_t)x * a.d;
+    const float* yr = c.Y ? c.Y + jq * a.d : a.X + (int64_t)y * a.d;
+    float acc = 0.f;
+    for (int t = 0; t < a.d; t++) {
+        float df = xr[t] - yr[t];
+        acc = fmaf(df, df, acc);
+    }
+    return sqrtf(acc);
+}
+
+template <bool EXPORT>
+__device__ __forceinline__ void emit(const FtArgs& a, uint32_t x, uint32_t y, uint32_t eta, uint32_t node) {
+    if (EXPORT) {
+        uint32_t idx = atomicAdd(a.flowcnt, 1u);
+        if ((int)idx < a.flow_cap) {
+            a.flow[4 * idx + 0] = x;
+            a.flow[4 * idx + 1] = y;
+            a.flow[4 * idx + 2] = eta;
+            a.flow[4 * idx + 3] = node;
+        }
+    }
+}
+
+// Northwest corner at one node.  A-list: doc item indices (a_list == null → identity 0..la),
+// B-list: query item indices (b_list == null → identity).  Adds the priced flow to `cost`.
+template <bool EXPORT>
+__device__ void nw_corner(const PairCtx& c, const uint16_t* a_list, int la, const uint16_t* b_list, int lb,
+                          uint32_t node, int lane, double& cost) {
+    uint32_t carry = 0;
+    for (int p0 = 0; p0 < la; p0 += 32) {
+        int p = p0 + lane;
+        uint32_t v = 0;
+        if (p < la) v = c.dres[a_list ? a_list[p] : p];
+        uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < la) c.dcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const uint32_t TA = carry;
+    carry = 0;
+    for (int p0 = 0; p0 < lb; p0 += 32) {
+        int p = p0 + lane;
+        uint32_t v = 0;
+        if (p < lb) v = c.qres[b_list ? b_list[p] : p];
+        uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < lb) c.qcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const uint32_t TB = carry;
+    __syncwarp();
+    const uint32_t T = TA < TB ? TA : TB;
+    if (T == 0) return;
+    for (int p = lane; p < la; p += 32) {
+        const uint32_t hi_a = c.dcum[p];
+        const uint32_t lo_a = p ? c.dcum[p - 1] : 0u;
+        const uint32_t end = hi_a < T ? hi_a : T;
+        if (lo_a >= end) continue;
+        // first j with qcum[j] > lo_a
+        int lo = 0, hi = lb;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (c.qcum[mid] > lo_a) hi = mid; else lo = mid + 1;
+        }
+        const int ia = a_list ? a_list[p] : p;
+        const uint32_t x = c.dvoc[ia] & FTI_VOCAB_MASK;
+        for (int j = lo; j < lb; j++) {
+            const uint32_t lo_b = j ? c.qcum[j - 1] : 0u;
+            if (lo_b >= end) break;
+            const uint32_t hi_b = c.qcum[j];
+            const uint32_t s0 = lo_b > lo_a ? lo_b : lo_a;
+            const uint32_t s1 = hi_b < end ? hi_b : end;
+            if (s1 > s0) {
+                const uint32_t eta = s1 - s0;
+                const int jq = b_list ? b_list[j] : j;
+                const uint32_t y = c.qitem[jq].x & FTI_VOCAB_MASK;
+                if (x != y) cost += (double)eta * (double)pair_dist(c, x, y, jq);
+                emit<EXPORT>(*c.a, x, y, eta, node);
+            }
+        }
+    }
+    __syncwarp();
+    for (int p = lane; p < la; p += 32) {
+        const uint32_t hi = c.dcum[p], lo = p ? c.dcum[p - 1] : 0u;
+        c.dres[a_list ? a_list[p] : p] = hi <= T ? 0u : hi - (lo > T ? lo : T);
+    }
+    for (int p = lane; p < lb; p += 32) {
+        const uint32_t hi = c.qcum[p], lo = p ? c.qcum[p - 1] : 0u;
+        c.qres[b_list ? b_list[p] : p] = hi <= T ? 0u : hi - (lo > T ? lo : T);
+    }
+    __syncwarp();
+}
+
+template <bool EXPORT>
+__global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int q = blockIdx.y;
+    const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
+    const QHeader* hdr = (const QHeader*)slot;
+    // shared layout: qitem[Sq] uint2 | vh[vh_cap] uint2 | Y[Sq*d] f32 (small d) | per-warp u32 arrays
+    uint2* qitem = (uint2*)smraw;
+    uint2* vh = qitem + a.Sq;
+    float* Y = (float*)(vh + a.L.vh_cap);
+    uint32_t* wbase = (uint32_t*)(Y + (a.small_d ? a.Sq * a.d : 0));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per_warp = 3 * a.Sd + 2 * a.Sq;
+    uint32_t* wsm = wbase + warp * per_warp;
+
+    const uint32_t sq = hdr->s, U = hdr->U, vh_mask = hdr->vh_mask, mh_mask = hdr->mh_mask;
+    const bool qok = hdr->err == 0 && sq > 0;
+    const uint2* gitems = (const uint2*)(slot + a.L.off_items);
+    const uint2* gvh = (const uint2*)(slot + a.L.off_vh);
+    const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
+    const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
+    for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) qitem[i] = gitems[i];
+    for (int i = threadIdx.x; i <= (int)vh_mask; i += blockDim.x) vh[i] = gvh[i];
+    if (a.small_d) {
+        for (int i = threadIdx.x; i < (int)sq * a.d; i += blockDim.x) {
+            int j = i / a.d, t = i - j * a.d;
+            Y[i] = a.X[(int64_t)(gitems[j].x & FTI_VOCAB_MASK) * a.d + t];
+        }
+    }
+    __syncthreads();
+
+    PairCtx c;
+    c.a = &a;
+    c.q = q;
+    c.qitem = qitem;
+    c.Y = a.small_d ? Y : nullptr;
+    c.dvoc = wsm;
+    c.dres = wsm + a.Sd;
+    c.dcum = wsm + 2 * a.Sd;
+    c.qres = wsm + 3 * a.Sd;
+    c.qcum = wsm + 3 * a.Sd + a.Sq;
+    c.trow_base = a.tab.table ? a.tab.table + (int64_t)q * a.tab.rows_cap * a.tab.ld : nullptr;
+    c.map = a.tab.map ? a.tab.map + (int64_t)q * a.N : nullptr;
+
+    const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
+    const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
+    for (int64_t dp = d0 + warp; dp < d1; dp += FT_WARPS) {
+        const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
+        double* outp = a.out ? a.out + (int64_t)q * a.out_ld + dp : nullptr;
+        if (!qok || doc < 0 || doc >= a.n) {
+            if (lane == 0 && outp) *outp = __longlong_as_double(0x7ff8000000000000ll);
+            if (lane == 0 && qok && doc >= a.n) atomicOr(a.err, FTI_ERR_RANGE);
+            continue;
+        }
+        const uint32_t i0 = a.doc_off[doc];
+        const int s = (int)(a.doc_off[doc + 1] - i0);
+        const uint32_t W = a.Wd[doc];
+        for (int i = lane; i < s; i += 32) {
+            const uint2 it = a.items[i0 + i];
+            c.dvoc[i] = it.x;
+            c.dres[i] = it.y * U;
+        }
+        for (int j = lane; j < (int)sq; j += 32) c.qres[j] = qitem[j].y * W;
+        __syncwarp();
+        double cost = 0.0;
+        // ---- phase A: self matches at singleton leaves ----
+        for (int i = lane; i < s; i += 32) {
+            const uint32_t v = c.dvoc[i];
+            if (v & FTI_FLAG_MULTI_LEAF) continue;
+            const uint32_t x = v & FTI_VOCAB_MASK;
+            uint32_t h = fti_hash(x) & vh_mask;
+            while (true) {
+                const uint2 e = vh[h];
+                if (e.x == x) {
+                    const uint32_t dr = c.dres[i], qr = c.qres[e.y];
+                    const uint32_t eta = dr < qr ? dr : qr;
+                    c.dres[i] = dr - eta;
+                    c.qres[e.y] = qr - eta;
+                    if (EXPORT && eta) emit<EXPORT>(a, x, x, eta, (uint32_t)a.path[(int64_t)x * a.cols + a.leaf_depth[x]]);
+                    break;
+                }
+                if (e.x == FTI_EMPTY) break;
+                h = (h + 1) & vh_mask;
+            }
+        }
+        __syncwarp();
+        // ---- phase B: common M-nodes, deepest first ----
+        const uint32_t m0 = a.mn_off[doc], m1 = a.mn_off[doc + 1];
+        if (m1 > m0 && hdr->n_mn > 0) {
+            for (uint32_t cb = m0; cb < m1; cb += 32) {
+                const uint32_t r = cb + lane;
+                uint4 rec = make_uint4(0, 0, 0, 0), qe = make_uint4(0, 0, 0, 0);
+                bool hit = false;
+                if (r < m1) {
+                    rec = a.mnodes[r];
+                    uint32_t h = fti_hash(rec.x) & mh_mask;
+                    while (true) {
+                        const uint4 e = gmh[h];
+                        if (e.x == rec.x) { qe = e; hit = true; break; }
+                        if (e.x == FTI_EMPTY) break;
+                        h = (h + 1) & mh_mask;
+                    }
+                }
+                unsigned hm = __ballot_sync(0xffffffffu, hit);
+                while (hm) {
+                    const int l = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const uint32_t node = __shfl_sync(0xffffffffu, rec.x, l);
+                    const uint32_t dlo = __shfl_sync(0xffffffffu, rec.y, l);
+                    const uint32_t dln = __shfl_sync(0xffffffffu, rec.z, l);
+                    const uint32_t qlo = __shfl_sync(0xffffffffu, qe.y, l);
+                    const uint32_t qln = __shfl_sync(0xffffffffu, qe.z, l);
+                    nw_corner<EXPORT>(c, a.mlists + dlo, (int)dln, gml + qlo, (int)qln, node, lane, cost);
+                }
+            }
+        }
+        // ---- phase C: the root ----
+        nw_corner<EXPORT>(c, nullptr, s, nullptr, (int)sq, 0u, lane, cost);
+        cost = fti_warp_sum_f64(cost);
+        if (lane == 0 && outp) *outp = cost / (double)((unsigned long long)W * U);
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                          const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
+                          int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap, cudaStream_t st) {
+    if (nq <= 0 || n_docs <= 0) return cudaSuccess;
+    const ft_index* ix = ds->ix;
+    FtArgs a{};
+    a.doc_off = ds->doc_off; a.items = ds->items; a.Wd = ds->W;
+    a.mn_off = ds->mn_off; a.mnodes = ds->mnodes; a.mlists = ds->mlists;
+    a.X = ix->X; a.d = ix->d; a.path = ix->path; a.cols = ix->d_star + 1; a.leaf_depth = ix->leaf_depth;
+    a.N = ix->N;
+    a.qblock = d_qblock; a.L = L; a.nq = nq;
+    a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs;
+    a.tab = tab;
+    a.out = d_out; a.out_ld = out_ld;
+    a.flow = d_flow; a.flowcnt = d_flowcnt; a.flow_cap = flow_cap;
+    a.Sd = ds->max_s;
+    a.Sq = L.smax;
+    a.n = ds->n;
+    a.err = ds->err_dev;
+    a.small_d = (tab.table == nullptr && ix->d <= FTI_SMALL_D) ? 1 : 0;
+    int64_t per_cta_target = std::max<int64_t>(FT_WARPS, (n_docs * nq + 148 * 16 - 1) / (148 * 16));
+    int64_t bx = std::max<int64_t>(1, (n_docs + per_cta_target - 1) / per_cta_target);
+    bx = std::max<int64_t>(bx, 1);
+    a.docs_per_cta = (n_docs + bx - 1) / bx;
+    bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
+    size_t smem = (size_t)a.Sq * 8 + (size_t)L.vh_cap * 8 + (a.small_d ? (size_t)a.Sq * a.d * 4 : 0) +
+                  (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
+    cudaError_t e;
+    if (d_flow) {
+        e = cudaFuncSetAttribute(k_flowtree<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_flowtree<true><<<dim3((unsigned)bx, (unsigned)nq), FT_WARPS * 32, smem, st>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_flowtree<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_flowtree<false><<<dim3((unsigned)bx, (unsigned)nq), FT_WARPS * 32, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}

@@ -1,0 +1,170 @@
+// ft_internal.cuh — shared internals of the B200 Flowtree library (NOT part of the C ABI).
+//
+// Layouts are described in DESIGN.md §6.  Nothing here is shared with oracle/ (DESIGN.md §4).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/flowtree.h"
+
+// ---------------------------------------------------------------------------------------------
+// limits
+// ---------------------------------------------------------------------------------------------
+#define FTI_MAX_SUPPORT 2048        // max support size of one distribution (doc or query)
+#define FTI_MAX_NODE_ENTRIES 8192   // max support * depth entries per distribution
+#define FTI_MAX_SELECT 8192         // max k / prefilter_m handled by the selection kernel
+#define FTI_MAX_WEIGHT_TOTAL 65535u // W, U <= 65535 keeps W*U < 2^32
+#define FTI_VOCAB_MASK 0x3FFFFFFFu  // vocab ids < 2^30; bits 30/31 of an item word are flags
+#define FTI_FLAG_MULTI_LEAF 0x80000000u  // the item's leaf holds >= 2 ground points
+#define FTI_FLAG_DEEP 0x40000000u        // some non-root node on the item's path holds >= 2 points
+#define FTI_SMALL_D 32              // d <= this: Flowtree prices distances on the fly (no table)
+#define FTI_EMPTY 0xFFFFFFFFu
+
+// device-side error bits (sticky, OR-ed into the dataset's mapped error word)
+#define FTI_ERR_RANGE 1u
+#define FTI_ERR_INVAL 2u
+#define FTI_ERR_OVERFLOW 4u
+#define FTI_ERR_CAP 8u
+
+// ---------------------------------------------------------------------------------------------
+// host-side error reporting
+// ---------------------------------------------------------------------------------------------
+ft_status fti_fail(ft_status st, const std::string& msg);
+#define FTI_CUDA(call)                                                                         \
+    do {                                                                                       \
+        cudaError_t _e = (call);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return fti_fail(FT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+// grow-only device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t reserve(size_t b) {
+        if (b <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t nb = b < 256 ? 256 : b;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e == cudaSuccess) bytes = nb;
+        return e;
+    }
+    template <class T>
+    T* as() const { return (T*)p; }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// ---------------------------------------------------------------------------------------------
+// index (a0): the quadtree, device resident
+// ---------------------------------------------------------------------------------------------
+struct ft_index {
+    int64_t N = 0;
+    int32_t d = 0;
+    int32_t D = 0;        // depth cap
+    int32_t d_star = 0;   // realised max leaf depth
+    int32_t l_root = 0;
+    double phi = 0.0;
+    int64_t M = 0;        // nodes
+    std::vector<double> sigma, mn;
+    std::vector<int64_t> level_base;   // first node id of each depth, size d_star+2
+    float* X = nullptr;               // [N*d]
+    int32_t* path = nullptr;          // [N*(d_star+1)], -1 below the leaf
+    uint8_t* leaf_depth = nullptr;    // [N]
+    uint8_t* node_depth = nullptr;    // [M]
+    int32_t* node_count = nullptr;    // [M] ground points in the cell
+    uint32_t* vflags = nullptr;       // [N] FTI_FLAG_* per ground point
+    int device = 0;
+};
+
+// ---------------------------------------------------------------------------------------------
+// dataset (a1): node-sorted layout in HBM
+// ---------------------------------------------------------------------------------------------
+struct QueryLayout {           // per-query slot geometry (host computed)
+    int32_t smax = 0;          // max support in the batch (rounded)
+    int32_t vh_cap = 0;        // vocab hash capacity (pow2)
+    int32_t nh_cap = 0;        // node hash capacity (pow2) — QT
+    int32_t mh_cap = 0;        // M-node hash capacity (pow2) — FT
+    int32_t ml_cap = 0;        // M-node list entries
+    size_t off_items = 0, off_vh = 0, off_nh = 0, off_nd = 0, off_mh = 0, off_ml = 0;
+    size_t stride = 0;         // bytes per query slot
+};
+
+struct QHeader {               // first 64 bytes of a query slot
+    uint32_t s;                // support size
+    uint32_t U;                // total weight
+    unsigned long long B;      // Σ_v ω(v) m_ν(v) over non-root nodes
+    uint32_t nh_mask;          // node hash mask (QT)
+    uint32_t vh_mask;          // vocab hash mask
+    uint32_t mh_mask;          // M-node hash mask (FT)
+    uint32_t n_nodes;          // distinct non-root nodes
+    uint32_t n_mn;             // M-nodes
+    uint32_t n_ml;             // M-node list entries
+    uint32_t err;              // FTI_ERR_* bits for this query
+    uint32_t pad[5];
+};
+static_assert(sizeof(QHeader) == 64, "QHeader is 64 bytes");
+
+struct ft_dataset {
+    const ft_index* ix = nullptr;
+    int64_t n = 0, nnz = 0;
+    int32_t max_s = 0;
+    int32_t max_mn = 0;        // max M-nodes per doc
+    // Flowtree record: items sorted by vocab id {vocab|flags, w}
+    uint32_t* doc_off = nullptr;   // [n+1]
+    uint2* items = nullptr;        // [nnz]
+    uint32_t* W = nullptr;         // [n]
+    // M-nodes (nodes holding >= 2 ground points) for the Flowtree phase B
+    uint32_t* mn_off = nullptr;    // [n+1]
+    uint4* mnodes = nullptr;       // {node, list_off(global), list_len, depth}, per doc (depth desc, node asc)
+    uint16_t* mlists = nullptr;    // item indices (vocab order) under each M-node
+    int64_t n_mn = 0, n_ml = 0;
+    // Quadtree record: non-root nodes sorted by id {node, mass}
+    uint32_t* qt_off = nullptr;    // [n+1]
+    uint2* qt = nullptr;
+    unsigned long long* A = nullptr;  // [n] Σ_v ω(v) m_μ(v)
+    int64_t n_qt = 0;
+    // sticky device-side error word (FTI_ERR_* bits)
+    uint32_t* err_dev = nullptr;
+    // scratch (grow-only; reused across calls)
+    DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist;
+};
+
+// ---------------------------------------------------------------------------------------------
+// cross-file launch helpers (host)
+// ---------------------------------------------------------------------------------------------
+QueryLayout fti_query_layout(const ft_index* ix, int32_t smax);
+cudaError_t fti_launch_query_prep(const ft_index* ix, const QueryLayout& L, const int64_t* d_qoff, int32_t nq,
+                                  const int32_t* d_qids, const uint32_t* d_qw, uint8_t* d_qblock,
+                                  uint32_t* d_err, cudaStream_t st);
+cudaError_t fti_launch_qt(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                          const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
+                          cudaStream_t st);
+struct FtTable {
+    const float* table = nullptr;   // [nq][rows_cap][ld] or null (on-the-fly distances)
+    const int32_t* map = nullptr;   // [nq][N] vocab -> row, or null (row = vocab)
+    int64_t rows_cap = 0;
+    int32_t ld = 0;
+};
+cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                          const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab,
+                          double* d_out, int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap,
+                          cudaStream_t st);
+cudaError_t fti_launch_dist_table(const ft_index* ix, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                                  const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap, float* d_table,
+                                  int32_t ld, cudaStream_t st);
+cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
+                                 int64_t n_cand, int32_t* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
+                                 cudaStream_t st);
+cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
+                              int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
+                              cudaStream_t st);

@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars: node paths, Quadtree values, flows and prefilter ids bit-exact; Flowtree
+values within 1e-5 relative (oracle 0 ⇒ GPU exactly 0); final top-k ids exact up to the tie band
+(oracle values within 2·tol of a rank boundary may permute among themselves).
+"""
+import concurrent.futures as cf
+
+import numpy as np
+import pytest
+
+import oracle
+import ft_testlib as H
+from conftest import get_workload
+
+pytestmark = pytest.mark.gpu
+
+FT_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ft():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_04126_b200 import build
+    build.build()
+    from paper_1910_04126_b200 import flowtree
+    return flowtree
+
+
+_TREES = {}
+
+
+def oracle_tree(wl):
+    key = (wl.name, wl.X.shape, wl.tree_seed, wl.max_depth)
+    if key not in _TREES:
+        _TREES[key] = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    return _TREES[key]
+
+
+def pmap(fn, items, workers=16):
+    with cf.ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(fn, items))
+
+
+def assert_ft_close(gpu, ref, what=""):
+    gpu = np.asarray(gpu, np.float64); ref = np.asarray(ref, np.float64)
+    zero = ref == 0.0
+    assert np.all(gpu[zero] == 0.0), f"{what}: oracle 0 but GPU nonzero"
+    rel = np.abs(gpu - ref) / np.maximum(np.abs(ref), 1e-300)
+    bad = np.nonzero(~zero & (rel > FT_TOL))[0]
+    assert bad.size == 0, f"{what}: {bad.size} values beyond tol, worst rel {rel[~zero].max():.3e}"
+
+
+def assert_topk_tieband(gpu_ids, gpu_vals, cand_ids, cand_oracle_vals, k, tol=FT_TOL, what=""):
+    """gpu top-k vs oracle ranking of the candidate set, allowing permutations inside tie bands."""
+    order = sorted(range(len(cand_ids)), key=lambda i: (cand_oracle_vals[i], cand_ids[i]))
+    ref_ids = [int(cand_ids[i]) for i in order][:k]
+    ref_vals = [float(cand_oracle_vals[i]) for i in order][:k]
+    val_of = {int(c): float(v) for c, v in zip(cand_ids, cand_oracle_vals)}
+    kk = min(k, len(cand_ids))
+    gids = [int(x) for x in gpu_ids[:kk]]
+    assert all(g in val_of for g in gids), f"{what}: id outside the candidate set"
+    assert len(set(gids)) == kk
+    for r in range(kk):
+        a, b = val_of[gids[r]], ref_vals[r]
+        assert abs(a - b) <= 2 * tol * max(abs(a), abs(b)), f"{what}: rank {r}: {gids[r]} vs {ref_ids[r]}"
+    # exact equality outside any band
+    if kk == k and kk < len(cand_ids):
+        boundary = ref_vals[-1]
+        band = {c for c, v in val_of.items() if abs(v - boundary) <= 2 * tol * abs(boundary)}
+        assert set(gids) - band == set(ref_ids) - band, f"{what}: top-k differs outside the tie band"
+    for t in range(kk, k):
+        assert gpu_ids[t] == -1 and np.isinf(gpu_vals[t])
+
+
+# ---------------------------------------------------------------------------------------------
+# a0 builder
+# ---------------------------------------------------------------------------------------------
+def _tree_equal(ft, X, seed=0, D=32, sigma=None):
+    T = oracle.Tree(X, seed=seed, max_depth=D, sigma=sigma)
+    ix = ft.Index(X, seed=seed, max_depth=D, sigma=sigma)
+    assert ix.phi == T.phi and ix.l_root == T.l_root and ix.d_star == T.d_star and ix.n_nodes == T.n_nodes
+    assert np.array_equal(ix.sigma(), T.sigma)
+    assert np.array_equal(ix.paths(), T.paths)
+    depth, count = ix.nodes()
+    assert np.array_equal(depth, T.node_depth) and np.array_equal(count, T.node_count)
+    return ix, T
+
+
+@pytest.mark.parametrize("fname", ["appendixA_example1.json", "appendixA_example2.json"])
+def test_builder_appendix(ft, fname):
+    g = H.golden(fname)
+    ix, _ = _tree_equal(ft, np.array(g["X"], np.float32), D=g["max_depth"], sigma=g["sigma"])
+    assert ix.paths().tolist() == g["paths"]
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_builder_random(ft, case):
+    rng = np.random.default_rng(50 + case)
+    N, d, D = [(1, 3, 8), (2, 1, 32), (40, 2, 4), (200, 3, 6), (65, 70, 32), (300, 8, 5), (100, 129, 32),
+               (50, 1, 52), (30, 2, 1), (500, 2, 32)][case]
+    if case in (3, 5):
+        X = rng.integers(0, 4, size=(N, d)).astype(np.float32)     # boundaries + duplicates
+    else:
+        X = rng.standard_normal((N, d)).astype(np.float32)
+    if case == 6:
+        X[10] = X[20]
+    sigma = None
+    if case == 3:
+        sigma = np.zeros(d)          # u reaches exactly 1: top-cell clamp
+    _tree_equal(ft, X, seed=1000 + case, D=D, sigma=sigma)
+
+
+def test_builder_degenerate(ft):
+    _tree_equal(ft, np.ones((7, 4), np.float32), seed=3)          # Φ = 0: a lone root leaf
+    _tree_equal(ft, np.zeros((1, 5), np.float32), seed=3)         # N = 1
+
+
+@pytest.mark.parametrize("name", ["tiny", "image", "text", "reviews"])
+def test_builder_configs(ft, name):
+    wl = get_workload(name, n_docs=64, n_queries=2)
+    T = oracle_tree(wl)
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    assert (ix.phi, ix.l_root, ix.d_star, ix.n_nodes) == (T.phi, T.l_root, T.d_star, T.n_nodes)
+    assert np.array_equal(ix.paths(), T.paths)
+
+
+# ---------------------------------------------------------------------------------------------
+# a1-a7 on small configs: every pair
+# ---------------------------------------------------------------------------------------------
+def _setup(ft, wl):
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    return ix, ds
+
+
+def _oracle_all(T, wl, which, pairs):
+    def one(p):
+        qi, di = p
+        a, aw = wl.doc(di)
+        b, bw = wl.query(qi)
+        return T.qt(a, aw, b, bw) if which == "qt" else T.ft(a, aw, b, bw)
+    return pmap(one, pairs)
+
+
+def test_tiny_all_pairs(ft):
+    wl = get_workload("tiny")
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    qt = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    fl = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    pairs = [(q, d) for q in range(wl.nq) for d in range(wl.n)]
+    ref_qt = _oracle_all(T, wl, "qt", pairs)
+    ref_ft = _oracle_all(T, wl, "ft", pairs)
+    assert np.array_equal(qt.ravel(), np.array([v for _, v in ref_qt]))           # bit-exact
+    assert_ft_close(fl.ravel(), ref_ft, "tiny FT")
+    for q, d in pairs:                                                               # every flow, bit-exact
+        b, bw = wl.query(q)
+        g = ds.flow(b, bw, d)
+        o = T.flow(*wl.doc(d), b, bw)
+        for key in ("src", "dst", "mass", "node"):
+            assert np.array_equal(g[key], o[key].astype(g[key].dtype)), (q, d, key)
+
+
+@pytest.mark.parametrize("name,n_docs,nq", [("image", 1500, 6), ("text", 1100, 5), ("reviews", 2600, 8)])
+def test_parity_subsets(ft, name, n_docs, nq):
+    """Several CTAs' worth of docs with a ragged tail; exact QT, FT within tol, sampled flows."""
+    wl = get_workload(name, n_docs=n_docs, n_queries=nq)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    qt = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    fl = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    rng = np.random.default_rng(7)
+    pairs = [(q, int(d)) for q in range(wl.nq) for d in rng.choice(wl.n, 150, replace=False)]
+    pairs += [(q, wl.n - 1) for q in range(wl.nq)]
+    ref_qt = _oracle_all(T, wl, "qt", pairs)
+    ref_ft = _oracle_all(T, wl, "ft", pairs)
+    assert np.array_equal(np.array([qt[q, d] for q, d in pairs]), np.array([v for _, v in ref_qt]))
+    assert_ft_close([fl[q, d] for q, d in pairs], ref_ft, f"{name} FT")
+    for q, d in pairs[:: max(1, len(pairs) // 40)]:
+        b, bw = wl.query(q)
+        g = ds.flow(b, bw, d)
+        o = T.flow(*wl.doc(d), b, bw)
+        assert np.array_equal(g["src"], o["src"]) and np.array_equal(g["dst"], o["dst"])
+        assert np.array_equal(g["mass"], o["mass"]) and np.array_equal(g["node"], o["node"])
+
+
+def test_doc_subset_and_self_queries(ft):
+    """docs subset argument; a query equal to a doc gives exactly 0 for both estimates."""
+    wl = get_workload("text", n_docs=300, n_queries=2)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    docs = np.array([5, 0, 299, 5, 17], np.int64)
+    a, aw = wl.doc(4)
+    b, bw = wl.doc(17)
+    q_off = np.array([0, len(a), len(a) + len(b)], np.int64)
+    q_ids = np.concatenate([a, b]); q_w = np.concatenate([aw, bw])
+    qt = ds.quadtree(q_off, q_ids, q_w, docs=docs)
+    fl = ds.flowtree(q_off, q_ids, q_w, docs=docs)
+    assert fl[1, 4] == 0.0 and qt[1, 4] == 0.0
+    for qi, (ids_, w_) in enumerate([(a, aw), (b, bw)]):
+        for j, dd in enumerate(docs):
+            assert qt[qi, j] == T.qt(*wl.doc(dd), ids_, w_)[1]
+            assert_ft_close([fl[qi, j]], [T.ft(*wl.doc(dd), ids_, w_)])
+
+
+# ---------------------------------------------------------------------------------------------
+# k-NN
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("prefilter_m", [0, 5, 30, 100, 1000])
+def test_knn_tiny(ft, prefilter_m):
+    wl = get_workload("tiny")
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    k = wl.k
+    ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, k, prefilter_m)
+    for q in range(wl.nq):
+        b, bw = wl.query(q)
+        ftv = [T.ft(*wl.doc(d), b, bw) for d in range(wl.n)]
+        if prefilter_m == 0 or prefilter_m >= wl.n:
+            cand = list(range(wl.n))
+        else:
+            qtv = [T.qt(*wl.doc(d), b, bw)[1] for d in range(wl.n)]
+            cand = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:prefilter_m]
+        assert_topk_tieband(ids[q], vals[q], cand, [ftv[c] for c in cand], k, what=f"q{q}")
+        assert_ft_close(vals[q], [ftv[i] for i in ids[q]])
+
+
+def test_knn_prefilter_ids_exact(ft):
+    """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id)."""
+    wl = get_workload("reviews", n_docs=5000, n_queries=4)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    m = 300
+    ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, m, m)
+    for q in range(wl.nq):
+        b, bw = wl.query(q)
+        qtv = pmap(lambda d: T.qt(*wl.doc(d), b, bw)[1], range(wl.n))
+        top = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:m]
+        assert set(ids[q].tolist()) == set(top)
+
+
+def test_knn_padding_and_errors(ft):
+    wl = get_workload("tiny", n_docs=7)
+    ix, ds = _setup(ft, wl)
+    ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 0)
+    assert np.all(ids[:, 7:] == -1) and np.all(np.isinf(vals[:, 7:]))
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 5)
+    assert e.value.status == ft.FT_EINVAL
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.quadtree(np.array([0, 2]), np.array([3, 3], np.int32), np.array([1, 1], np.uint32))
+    assert e.value.status == ft.FT_EINVAL                    # duplicate id
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.quadtree(np.array([0, 1]), np.array([5000], np.int32), np.array([1], np.uint32))
+    assert e.value.status == ft.FT_ERANGE
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.flowtree(np.array([0, 1]), np.array([3], np.int32), np.array([70000], np.uint32))
+    assert e.value.status == ft.FT_EOVERFLOW
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.flowtree(np.array([0, 0]), np.array([], np.int32), np.array([], np.uint32))
+    assert e.value.status == ft.FT_EINVAL                    # empty query
+    with pytest.raises(ft.FlowtreeError) as e:
+        ft.Dataset(ix, np.array([0, 2]), np.array([1, 1], np.int32), np.array([1, 1], np.uint32))
+    assert e.value.status == ft.FT_EINVAL and "document 0" in str(e.value)
+    with pytest.raises(ft.FlowtreeError) as e:
+        ft.Dataset(ix, np.array([0, 1, 2]), np.array([1, 1000], np.int32), np.array([1, 1], np.uint32))
+    assert e.value.status == ft.FT_ERANGE and "document 1" in str(e.value)
+
+
+def test_device_pointers_async_and_sticky_error(ft):
+    import torch
+    wl = get_workload("tiny")
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    dev = torch.device("cuda:0")
+    qi = torch.from_numpy(wl.q_ids).to(dev)
+    qw = torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32)
+    out = torch.empty((wl.nq, wl.n), dtype=torch.float64, device=dev)
+    ds.quadtree(wl.q_off, qi, qw, out=out)
+    ds.synchronize(torch.cuda.current_stream())
+    host = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    assert np.array_equal(out.cpu().numpy(), host)
+    oid = torch.empty((wl.nq, 5), dtype=torch.int64, device=dev)
+    ov = torch.empty((wl.nq, 5), dtype=torch.float64, device=dev)
+    ds.knn(wl.q_off, qi, qw, 5, 0, out_ids=oid, out_val=ov)
+    hid, hv = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 5, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(oid.cpu().numpy(), hid) and np.array_equal(ov.cpu().numpy(), hv)
+    # a bad vocab id on the device is reported by the next ft_synchronize
+    bad = qi.clone(); bad[0] = 10**6
+    ds.quadtree(wl.q_off, bad, qw, out=out)
+    with pytest.raises(ft.FlowtreeError) as e:
+        ds.synchronize(torch.cuda.current_stream())
+    assert e.value.status == ft.FT_ERANGE
+    assert torch.isnan(out[0]).all()
+    ds.synchronize(torch.cuda.current_stream())          # cleared
+
+
+# ---------------------------------------------------------------------------------------------
+# full size (BASELINE configs, the bench's launch configuration), sampled against the oracle
+# ---------------------------------------------------------------------------------------------
+def test_reviews_full_size_sampled(ft):
+    import torch
+    wl = get_workload("reviews", n_queries=1000)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    dev = torch.device("cuda:0")
+    qi = torch.from_numpy(wl.q_ids).to(dev)
+    qw = torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32)
+    out = torch.empty((wl.nq, wl.n), dtype=torch.float64, device=dev)
+    ds.quadtree(wl.q_off, qi, qw, out=out)
+    ds.synchronize(torch.cuda.current_stream())
+    rng = np.random.default_rng(11)
+    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, wl.nq, 600), rng.integers(0, wl.n, 600))]
+    pairs += [(wl.nq - 1, wl.n - 1), (0, 0)]
+    ref = _oracle_all(T, wl, "qt", pairs)
+    got = out.cpu().numpy()
+    assert np.array_equal(np.array([got[q, d] for q, d in pairs]), np.array([v for _, v in ref]))
+    # Flowtree over all 100k docs for 8 queries, sampled
+    sub = wl.subset_queries(8)
+    fl = ds.flowtree(sub.q_off, sub.q_ids, sub.q_w)
+    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, 8, 300), rng.integers(0, wl.n, 300))]
+    assert_ft_close([fl[q, d] for q, d in pairs], _oracle_all(T, sub, "ft", pairs), "reviews FT")
+    # k-NN with the BASELINE prefilter, 6 queries, against the oracle pipeline
+    sub = wl.subset_queries(6)
+    ids, vals = ds.knn(sub.q_off, sub.q_ids, sub.q_w, wl.k, wl.prefilter_m)
+    for q in range(sub.nq):
+        b, bw = sub.query(q)
+        qtv = pmap(lambda d: T.qt(*wl.doc(d), b, bw)[1], range(wl.n))
+        cand = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:wl.prefilter_m]
+        ftv = pmap(lambda d: T.ft(*wl.doc(d), b, bw), cand)
+        assert_topk_tieband(ids[q], vals[q], cand, ftv, wl.k, what=f"reviews q{q}")
