@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py — Flowtree k-NN hot path on B200 (BASELINE.json metric, reviews-like config).
+
+One step = one pass of the whole hot path over one batch of queries:
+ft_knn(queries, k=10, prefilter_m=1000) = query prep → Quadtree over all n=100k docs → top-1000
+→ distance table → Flowtree rerank → top-10, through the C ABI with inputs already in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank holds the dataset and answers its own
+batch of queries — the path shards by query with no data-path collective, so
+scaling is weak; the device time is the max over ranks (NCCL all-reduce of the timings only).
+Prints one JSON line on rank 0.  --impl reference times the CPU oracle (the only other place
+this file runs oracle/) on the same config, metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Flowtree (query,doc) estimates/sec and k-NN queries/sec at n=100k; % of HBM roofline"
+CONFIG = "reviews"
+WORKLOAD = "reviews-like (BASELINE configs[2]): X 100k x R^300 mixture, n=100k docs, s~U{10..90}, Zipf(1.1) ids"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM-style copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def oracle_knn_rate(wl, tree, qsel, threads):
+    """Oracle k-NN pipeline (QT over all docs -> top-m -> FT -> top-k) for the queries qsel, one
+    query per host thread.  Returns (queries/s, wall seconds)."""
+    def one(q):
+        b, bw = wl.query(q)
+        return tree.knn(wl.doc_off, wl.ids, wl.w, b, bw, wl.k, wl.prefilter_m)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, qsel))
+    dt = time.perf_counter() - t0
+    return len(qsel) / dt, dt
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return 0                                   # rank 0 alone runs the CPU oracle
+    import oracle
+    from paper_1910_04126_b200 import workloads
+    wl = workloads.make(CONFIG)
+    tree = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    threads = os.cpu_count() or 1
+    per_step = max(threads, 16)
+    rng = np.random.default_rng(0)
+    times = []
+    for s in range(args.warmup + args.steps):
+        qsel = rng.choice(wl.nq, per_step, replace=False)
+        rate, dt = oracle_knn_rate(wl, tree, qsel, threads)
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = per_step * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "n": wl.n, "queries_per_step": per_step,
+                                         "k": wl.k, "prefilter_m": wl.prefilter_m},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{per_step} random queries per step x full n={wl.n}, "
+                                   f"QT->top-{wl.prefilter_m}->FT->top-{wl.k}, one query per host thread"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    rank, world, local = dist_info()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_1910_04126_b200 import flowtree as ft, workloads
+
+    Q = args.queries
+    wl_all = workloads.make(CONFIG, n_queries=Q * world)
+    a, b = int(wl_all.q_off[rank * Q]), int(wl_all.q_off[(rank + 1) * Q])
+    q_off = (wl_all.q_off[rank * Q:(rank + 1) * Q + 1] - a).astype(np.int64)
+    q_ids_h, q_w_h = wl_all.q_ids[a:b], wl_all.q_w[a:b]
+    wl = wl_all
+    k, m = wl.k, wl.prefilter_m
+
+    t_build = time.perf_counter()
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    t_load = time.perf_counter()
+    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    t_done = time.perf_counter()
+    build_s, load_s = t_load - t_build, t_done - t_load
+
+    stream = torch.cuda.current_stream()
+    q_ids = torch.from_numpy(q_ids_h).to(dev)
+    q_w = torch.from_numpy(q_w_h.view(np.int32)).to(dev).view(torch.uint32)
+    out_ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
+    out_val = torch.empty((Q, k), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        ds.knn(q_off, q_ids, q_w, k, m, out_ids=out_ids, out_val=out_val, stream=stream)
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    ds.synchronize(stream)
+    ft.ft_profile_enable(ds.h, True)
+    ft.ft_profile_reset(ds.h)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ft.ft_launch_count()
+    clocks = ClockSampler(local)
+    barrier_sync()
+    for i in range(args.steps):
+        flush.zero_()                         # L2 flush (512 MiB write > 126 MB L2), outside the events
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    barrier_sync()
+    clk = clocks.stop()
+    launches = (ft.ft_launch_count() - launches0) / args.steps
+    ds.synchronize(stream)
+    t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    stages = ft.profile_dict(ds.h)
+    ft.ft_profile_enable(ds.h, False)
+    if dist is not None:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    value = world * Q * args.steps / (t_ms / 1e3)
+
+    # ---- dominant kernel of the step and its live roofline ----
+    peak, peak_src = measured_peaks()
+    n_qt = ds.n_qt
+    qt_bytes = Q * (8 * n_qt + 16 * ds.n)        # 8 B per doc tree node + 16 B per doc, per query scan
+    dom = max(stages.items(), key=lambda kv: kv[1][0])
+    qt_ms, qt_n = stages["quadtree"]
+    qt_avg = qt_ms / max(qt_n, 1)
+    achieved = qt_bytes / (qt_avg / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("k_qt_dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": "k_qt (Quadtree estimate, a3)", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": qt_bytes, "launch_ms": qt_avg, "peak_source": peak_src,
+                "dominant_stage": dom[0]}
+
+    # ---- kernel-level numbers over all n docs (separately timed; not part of the step) ----
+    kernels = {}
+    if not args.no_kernels:
+        out_qt = torch.empty((Q, ds.n), dtype=torch.float64, device=dev)
+        for _ in range(2):
+            ds.quadtree(q_off, q_ids, q_w, out=out_qt, stream=stream)
+        ft.ft_profile_enable(ds.h, True)
+        ft.ft_profile_reset(ds.h)
+        reps = 3
+        for _ in range(reps):
+            flush.zero_()
+            ds.quadtree(q_off, q_ids, q_w, out=out_qt, stream=stream)
+        st = ft.profile_dict(ds.h)
+        qms = st["quadtree"][0] / reps
+        del out_qt
+        kernels["quadtree_all_docs"] = {
+            "pairs": Q * ds.n, "ms": qms, "pairs_per_s": Q * ds.n / (qms / 1e3),
+            "algorithmic_GBps": qt_bytes / (qms / 1e3) / 1e9, "frac_hbm": qt_bytes / (qms / 1e3) / 1e9 / peak}
+        nqf = min(Q, args.ft_queries)
+        sub_off = q_off[:nqf + 1]
+        e = int(sub_off[-1])
+        out_ft = torch.empty((nqf, ds.n), dtype=torch.float64, device=dev)
+        ds.flowtree(sub_off, q_ids[:e], q_w[:e], out=out_ft, stream=stream)
+        ft.ft_profile_reset(ds.h)
+        flush.zero_()
+        ds.flowtree(sub_off, q_ids[:e], q_w[:e], out=out_ft, stream=stream)
+        st = ft.profile_dict(ds.h)
+        ft.ft_profile_enable(ds.h, False)
+        fms, tms = st["flowtree"][0], st["dist_table"][0]
+        ft_bytes = nqf * (8 * ds.nnz + 16 * ds.n)      # 8 B per doc support point + 16 B per doc
+        kernels["flowtree_all_docs"] = {
+            "queries": nqf, "pairs": nqf * ds.n, "ms_flowtree_kernel": fms, "ms_dist_table": tms,
+            "pairs_per_s": nqf * ds.n / (fms / 1e3), "algorithmic_GBps": ft_bytes / (fms / 1e3) / 1e9,
+            "frac_hbm": ft_bytes / (fms / 1e3) / 1e9 / peak,
+            "pairs_per_s_incl_table": nqf * ds.n / ((fms + tms) / 1e3)}
+        del out_ft
+
+    # ---- e2e: same metric through the C ABI with pinned HOST buffers ----
+    qi_pin = torch.from_numpy(q_ids_h.copy()).pin_memory()
+    qw_pin = torch.from_numpy(q_w_h.view(np.int32).copy()).pin_memory().view(torch.uint32)
+    oi_pin = torch.empty((Q, k), dtype=torch.int64).pin_memory()
+    ov_pin = torch.empty((Q, k), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        ds.knn(q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream)
+    barrier_sync()
+    e_ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ds.knn(q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        e_ms += e0.elapsed_time(e1)
+    barrier_sync()
+    if dist is not None:
+        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    h2d = 8 * (Q + 1) + 4 * len(q_ids_h) + 4 * len(q_w_h)
+    d2h = Q * k * (8 + 8)
+    e2e = {"value": world * Q * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h}
+
+    # ---- CPU baseline: the oracle, rank 0 at N=1 only, bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        tree = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+        threads = os.cpu_count() or 1
+        nsamp = max(16, threads * 2)
+        rate, dt = oracle_knn_rate(wl, tree, list(range(nsamp)), threads)
+        cpu = {"value": rate, "unit": "queries/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {nsamp} queries x full n={wl.n}, QT->top-{m}->FT->top-{k}, one query per host "
+                         f"thread ({dt:.1f} s wall)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64/f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": ds.n, "N": wl.X.shape[0], "d": wl.X.shape[1],
+                       "queries_per_rank": Q, "global_batch": Q * world, "k": k, "prefilter_m": m,
+                       "parallelism": f"query-sharded x{world}", "l2": "flushed (512 MiB write) between timed steps",
+                       "qt_records": int(n_qt), "nnz": int(ds.nnz)},
+            "ft_estimates_per_s": kernels.get("flowtree_all_docs", {}).get("pairs_per_s"),
+            "qt_estimates_per_s": kernels.get("quadtree_all_docs", {}).get("pairs_per_s"),
+            "roofline": roofline, "kernels": kernels,
+            "stages_ms_per_step": {s: v[0] / args.steps for s, v in stages.items()},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+            "build_s": build_s, "load_s": load_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--queries", type=int, default=1000, help="queries per rank per step")
+    p.add_argument("--ft-queries", type=int, default=64, help="queries for the exhaustive Flowtree kernel line")
+    p.add_argument("--no-kernels", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -117,6 +117,20 @@ ft_status ft_knn(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const i
 /* Synchronise `stream` and report (then clear) any sticky device-side validation error.      */
 ft_status ft_synchronize(const ft_dataset* ds, void* stream);
 
+/* Diagnostics (used by bench.py for the live roofline numbers).  With profiling enabled, the
+ * query calls on `ds` record a CUDA event pair around every stage on the call's stream; reading
+ * synchronises the events and returns, per stage, the total device milliseconds and the number
+ * of timed launches since the last reset.  Stages: 0 query prep (a2), 1 Quadtree (a3),
+ * 2 top-m select (a4), 3 candidate vocabulary (a5 prep), 4 distance table (a5), 5 Flowtree (a6),
+ * 6 top-k select (a7).  ft_launch_count() is the number of kernels this library has launched
+ * in the process so far.                                                                      */
+#define FT_NUM_STAGES 7
+ft_status ft_profile_enable(ft_dataset* ds, int32_t enable);
+ft_status ft_profile_reset(ft_dataset* ds);
+ft_status ft_profile_read(ft_dataset* ds, int32_t stage, double* total_ms, int64_t* launches);
+const char* ft_profile_stage_name(int32_t stage);
+uint64_t ft_launch_count(void);
+
 void ft_index_free(ft_index* ix);
 void ft_dataset_free(ft_dataset* ds);
 /* Thread-local message of the last failing call on this thread ("" if none).                 */

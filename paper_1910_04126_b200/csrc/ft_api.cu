@@ -8,16 +8,50 @@
 
 #include "ft_device.cuh"
 
+#include <atomic>
+
 static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
 
 ft_status fti_fail(ft_status st, const std::string& msg) {
     g_last_error = msg;
     return st;
 }
 
+void fti_count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
 extern "C" const char* ft_last_error(void) { return g_last_error.c_str(); }
+extern "C" uint64_t ft_launch_count(void) { return g_launches.load(); }
 
 namespace {
+
+// records a CUDA event pair around one stage when profiling is enabled on the dataset
+struct StageTimer {
+    ft_dataset* ds;
+    int stage;
+    cudaStream_t st;
+    cudaEvent_t b = nullptr;
+    StageTimer(ft_dataset* d, int s, cudaStream_t t) : ds(d), stage(s), st(t) {
+        if (!ds->prof) return;
+        cudaEvent_t a = take();
+        b = take();
+        cudaEventRecord(a, st);
+        ds->prof_pending.push_back({stage, a, b});
+    }
+    ~StageTimer() {
+        if (b) cudaEventRecord(b, st);
+    }
+    cudaEvent_t take() {
+        if (!ds->prof_pool.empty()) {
+            cudaEvent_t e = ds->prof_pool.back();
+            ds->prof_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
 
 bool is_device_ptr(const void* p) {
     if (!p) return false;
@@ -119,6 +153,7 @@ ft_status stage_queries(ft_dataset* ds, const int64_t* q_off, int32_t nq, const 
     }
     FTI_RES(ds->s_qblock, S.L.stride * (size_t)nq);
     S.qblock = ds->s_qblock.as<uint8_t>();
+    StageTimer tm(ds, FTI_ST_PREP, st);
     FTI_CUDA(fti_launch_query_prep(ix, S.L, S.qoff_dev, nq, S.qids, S.qw, S.qblock, ds->err_dev, st));
     return FT_OK;
 }
@@ -152,6 +187,7 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
                          int64_t n_docs, double* d_out, int64_t out_ld, cudaStream_t st) {
     const ft_index* ix = ds->ix;
     if (ix->d <= FTI_SMALL_D) {
+        StageTimer tm(ds, FTI_ST_FT, st);
         FTI_CUDA(fti_launch_ft(ds, S.L, S.qblock, nq, d_docs, docs_ld, n_docs, FtTable{}, d_out, out_ld, nullptr,
                                nullptr, 0, st));
         return FT_OK;
@@ -177,13 +213,18 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         tab.rows_cap = rows_cap;
         tab.ld = ld;
         if (use_map) {
+            StageTimer tm(ds, FTI_ST_VMAP, st);
             FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<int32_t>(),
                                           ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap, st));
             tab.map = ds->s_map.as<int32_t>();
         }
-        FTI_CUDA(fti_launch_dist_table(ix, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
-                                       use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
-                                       ds->s_table.as<float>(), ld, st));
+        {
+            StageTimer tm(ds, FTI_ST_DIST, st);
+            FTI_CUDA(fti_launch_dist_table(ix, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
+                                           use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
+                                           ds->s_table.as<float>(), ld, st));
+        }
+        StageTimer tm(ds, FTI_ST_FT, st);
         FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,
                                nullptr, nullptr, 0, st));
     }
@@ -214,6 +255,7 @@ ft_status estimate_common(const ft_dataset* cds, const int64_t* q_off, int32_t n
         rc = flowtree_stage(ds, S, nq, d_docs, 0, nd, d_out, nd, st);
         if (rc) return rc;
     } else {
+        StageTimer tm(ds, FTI_ST_QT, st);
         FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, d_docs, 0, nd, d_out, nd, st));
     }
     if (!dev_out) {
@@ -325,17 +367,25 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
         FTI_RES(ds->s_vals, sizeof(double) * nq * n);
         rc = flowtree_stage(ds, S, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st);
         if (rc) return rc;
+        StageTimer tm(ds, FTI_ST_SELK, st);
         FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, k, d_ids, d_val, k, st));
     } else {
         const int64_t m = prefilter_m;
         FTI_RES(ds->s_vals, sizeof(double) * nq * n);
         FTI_RES(ds->s_cand, sizeof(int64_t) * nq * m);
         FTI_RES(ds->s_vals2, sizeof(double) * nq * m);
-        FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st));
-        FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m, ds->s_cand.as<int64_t>(),
-                                   ds->s_vals2.as<double>(), m, st));
+        {
+            StageTimer tm(ds, FTI_ST_QT, st);
+            FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st));
+        }
+        {
+            StageTimer tm(ds, FTI_ST_SELM, st);
+            FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m,
+                                       ds->s_cand.as<int64_t>(), ds->s_vals2.as<double>(), m, st));
+        }
         rc = flowtree_stage(ds, S, nq, ds->s_cand.as<int64_t>(), m, m, ds->s_vals2.as<double>(), m, st);
         if (rc) return rc;
+        StageTimer tm(ds, FTI_ST_SELK, st);
         FTI_CUDA(fti_launch_select(ds->s_vals2.as<double>(), m, ds->s_cand.as<int64_t>(), m, m, nq, k, d_ids, d_val,
                                    k, st));
     }
@@ -350,4 +400,47 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
 extern "C" ft_status ft_synchronize(const ft_dataset* ds, void* stream) {
     if (!ds) return fti_fail(FT_ESTATE, "ft_synchronize: NULL dataset");
     return check_device_errors(ds, (cudaStream_t)stream, "ft_synchronize");
+}
+
+extern "C" ft_status ft_profile_enable(ft_dataset* ds, int32_t enable) {
+    if (!ds) return fti_fail(FT_ESTATE, "ft_profile_enable: NULL dataset");
+    ds->prof = enable != 0;
+    return FT_OK;
+}
+
+static ft_status profile_drain(ft_dataset* ds) {
+    for (auto& p : ds->prof_pending) {
+        FTI_CUDA(cudaEventSynchronize(p.b));
+        float ms = 0.f;
+        FTI_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        ds->prof_ms[p.stage] += ms;
+        ds->prof_n[p.stage] += 1;
+        ds->prof_pool.push_back(p.a);
+        ds->prof_pool.push_back(p.b);
+    }
+    ds->prof_pending.clear();
+    return FT_OK;
+}
+
+extern "C" ft_status ft_profile_reset(ft_dataset* ds) {
+    if (!ds) return fti_fail(FT_ESTATE, "ft_profile_reset: NULL dataset");
+    ft_status rc = profile_drain(ds);
+    for (int s = 0; s < FT_NUM_STAGES; s++) { ds->prof_ms[s] = 0; ds->prof_n[s] = 0; }
+    return rc;
+}
+
+extern "C" ft_status ft_profile_read(ft_dataset* ds, int32_t stage, double* total_ms, int64_t* launches) {
+    if (!ds) return fti_fail(FT_ESTATE, "ft_profile_read: NULL dataset");
+    if (stage < 0 || stage >= FT_NUM_STAGES) return fti_fail(FT_EINVAL, "ft_profile_read: bad stage");
+    ft_status rc = profile_drain(ds);
+    if (rc) return rc;
+    if (total_ms) *total_ms = ds->prof_ms[stage];
+    if (launches) *launches = ds->prof_n[stage];
+    return FT_OK;
+}
+
+extern "C" const char* ft_profile_stage_name(int32_t stage) {
+    static const char* names[FT_NUM_STAGES] = {"query_prep", "quadtree", "select_m", "vocab_map",
+                                               "dist_table", "flowtree", "select_k"};
+    return (stage >= 0 && stage < FT_NUM_STAGES) ? names[stage] : "";
 }

@@ -135,6 +135,7 @@ cudaError_t fti_launch_dist_table(const ft_index* ix, const QueryLayout& L, cons
     if (nq <= 0 || rows_cap <= 0) return cudaSuccess;
     dim3 grid((unsigned)((rows_cap + TR - 1) / TR), (unsigned)nq);
     k_dist_table<<<grid, 256, 0, st>>>(ix->X, ix->d, d_qblock, L, d_rows, d_rowcnt, rows_cap, d_table, ld);
+    fti_count_launches(1);
     return cudaGetLastError();
 }
 
@@ -150,5 +151,6 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
         k_mark<<<g, 256, 0, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, N, d_map);
     }
     k_compact<<<nq, 1024, 0, st>>>(N, d_map, d_rows, d_rowcnt, rows_cap);
+    fti_count_launches(n_cand > 0 ? 2 : 1);
     return cudaGetLastError();
 }

@@ -331,5 +331,6 @@ cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint
         if (e != cudaSuccess) return e;
         k_flowtree<false><<<dim3((unsigned)bx, (unsigned)nq), FT_WARPS * 32, smem, st>>>(a);
     }
+    fti_count_launches(1);
     return cudaGetLastError();
 }

@@ -134,6 +134,13 @@ struct ft_dataset {
     int64_t n_qt = 0;
     // sticky device-side error word (FTI_ERR_* bits)
     uint32_t* err_dev = nullptr;
+    // per-stage profiling (ft_profile_*)
+    bool prof = false;
+    struct EvPair { int stage; cudaEvent_t a, b; };
+    std::vector<EvPair> prof_pending;
+    std::vector<cudaEvent_t> prof_pool;
+    double prof_ms[FT_NUM_STAGES] = {0};
+    int64_t prof_n[FT_NUM_STAGES] = {0};
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
     DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist;
@@ -142,6 +149,8 @@ struct ft_dataset {
 // ---------------------------------------------------------------------------------------------
 // cross-file launch helpers (host)
 // ---------------------------------------------------------------------------------------------
+void fti_count_launches(int n);
+enum { FTI_ST_PREP = 0, FTI_ST_QT, FTI_ST_SELM, FTI_ST_VMAP, FTI_ST_DIST, FTI_ST_FT, FTI_ST_SELK };
 QueryLayout fti_query_layout(const ft_index* ix, int32_t smax);
 cudaError_t fti_launch_query_prep(const ft_index* ix, const QueryLayout& L, const int64_t* d_qoff, int32_t nq,
                                   const int32_t* d_qids, const uint32_t* d_qw, uint8_t* d_qblock,

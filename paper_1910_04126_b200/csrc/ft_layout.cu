@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(256) k_layout(LayoutArgs a) {
     __shared__ unsigned int s_W;
     __shared__ int mn_hist[64];
     __shared__ int mn_lt[64], mn_gt[64];
-    __shared__ int s_nseg, s_nmn, s_nml;
 
     const int64_t doc = blockIdx.x;
     const uint32_t base = a.off[doc];
@@ -223,8 +222,6 @@ __global__ void __launch_bounds__(256) k_layout(LayoutArgs a) {
         for (int e = e0; e < e1; e++) a.mlists[lo + lofs + (e - e0)] = (uint16_t)(uint32_t)key_ent[e];
     }
 }
-
-inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 const char* err_name(uint32_t e) {
     if (e & FTI_ERR_RANGE) return "vocab id outside [0, N)";

@@ -161,5 +161,6 @@ cudaError_t fti_launch_qt(const ft_dataset* ds, const QueryLayout& L, const uint
     cudaError_t e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_qt<<<dim3((unsigned)bx, (unsigned)qchunks), QT_WARPS * 32, smem, st>>>(a);
+    fti_count_launches(1);
     return cudaGetLastError();
 }

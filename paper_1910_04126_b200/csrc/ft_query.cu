@@ -240,5 +240,6 @@ cudaError_t fti_launch_query_prep(const ft_index* ix, const QueryLayout& L, cons
     cudaError_t e = cudaFuncSetAttribute(k_query_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (nq > 0) k_query_prep<<<nq, 256, smem, st>>>(a);
+    fti_count_launches(nq > 0 ? 1 : 0);
     return cudaGetLastError();
 }

@@ -137,5 +137,6 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P);
+    fti_count_launches(1);
     return cudaGetLastError();
 }

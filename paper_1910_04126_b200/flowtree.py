@@ -25,7 +25,10 @@ STATUS_NAMES = {0: "FT_OK", 1: "FT_EINVAL", 2: "FT_ERANGE", 3: "FT_EOVERFLOW", 4
 EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft_index_paths",
             "ft_index_sigma", "ft_index_nodes", "ft_load_dataset", "ft_dataset_info",
             "ft_quadtree_estimate", "ft_flowtree_estimate", "ft_flowtree_flow", "ft_knn",
-            "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error"]
+            "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error",
+            "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_stage_name",
+            "ft_launch_count"]
+FT_NUM_STAGES = 7
 
 
 class FlowtreeError(RuntimeError):
@@ -59,6 +62,11 @@ def _load_lib():
         "ft_index_free": (None, [P]),
         "ft_dataset_free": (None, [P]),
         "ft_last_error": (ctypes.c_char_p, []),
+        "ft_profile_enable": (st, [P, i32]),
+        "ft_profile_reset": (st, [P]),
+        "ft_profile_read": (st, [P, i32, P, P]),
+        "ft_profile_stage_name": (ctypes.c_char_p, [i32]),
+        "ft_launch_count": (u64, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -242,6 +250,34 @@ def ft_dataset_free(ds):
 
 def ft_last_error() -> str:
     return _lib.ft_last_error().decode()
+
+
+def ft_profile_enable(ds, enable: bool = True):
+    _check(_lib.ft_profile_enable(ds, 1 if enable else 0))
+
+
+def ft_profile_reset(ds):
+    _check(_lib.ft_profile_reset(ds))
+
+
+def ft_profile_read(ds, stage: int):
+    """(total device ms, timed launches) of one stage since the last reset."""
+    ms = ctypes.c_double(); n = ctypes.c_int64()
+    _check(_lib.ft_profile_read(ds, stage, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
+def ft_profile_stage_name(stage: int) -> str:
+    return _lib.ft_profile_stage_name(stage).decode()
+
+
+def ft_launch_count() -> int:
+    return int(_lib.ft_launch_count())
+
+
+def profile_dict(ds):
+    """{stage name: (total ms, launches)} for every stage."""
+    return {ft_profile_stage_name(s): ft_profile_read(ds, s) for s in range(FT_NUM_STAGES)}
 
 
 # ------------------------------------------------------------------------------------------------
