@@ -143,7 +143,7 @@ struct ft_dataset {
     int64_t prof_n[FT_NUM_STAGES] = {0};
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -155,7 +155,7 @@ QueryLayout fti_query_layout(const ft_index* ix, int32_t smax);
 cudaError_t fti_launch_query_prep(const ft_index* ix, const QueryLayout& L, const int64_t* d_qoff, int32_t nq,
                                   const int32_t* d_qids, const uint32_t* d_qw, uint8_t* d_qblock,
                                   uint32_t* d_err, cudaStream_t st);
-cudaError_t fti_launch_qt(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
                           cudaStream_t st);
 struct FtTable {

@@ -4,27 +4,198 @@
 //   num = Σ_{v≠root} ω(v) |U m_μ(v) − W m_ν(v)|
 //       = U·A + W·B − 2 Σ_{v ∈ nodes(μ) ∩ nodes(ν)} ω(v) min(U m_μ(v), W m_ν(v))
 //   QT  = (num · 2^{ℓ_root − D*}) / (W·U)
-// so the kernel streams the doc's node-sorted record (the sparse ℓ1 embedding)
-// once, probes each record against the query node hashes staged in shared memory, and only the
-// common nodes contribute.  The numerator is an exact u64; the value takes two correctly
-// rounded FP64 operations, so it is bit-identical to the oracle.
+// so the kernel streams each doc's node-sorted record (the sparse ℓ1 embedding,
+// PAPER.md:131-134) once per chunk of 32 queries and only the common nodes contribute.  The
+// numerator is an exact u64; the value takes two correctly rounded FP64 operations, so it is
+// bit-identical to the oracle.
 //
-// Mapping: a CTA stages QC queries' node hashes in shared memory and streams a contiguous doc
-// range; one warp per doc, lane-strided 8-byte records (coalesced); per-warp shared u64
-// accumulators per query (hits are rare at d = 300, so atomics do not contend).
+// Query-chunk structure (k_qt_chunk, one CTA per chunk of ≤ 32 queries): one open-addressing hash
+// over the union of the chunk's query nodes; each distinct node carries a 32-bit mask of the
+// chunk queries that contain it and an offset into a posting array of packed
+// (m_ν(v) | depth << 16 | query << 24) words ordered by query.
+//
+// Doc scan (k_qt, grid = doc tiles × chunks): the chunk structure is staged in shared memory;
+// one warp per doc, lane-strided 8-byte records (coalesced), one probe per record; for every hit
+// the warp visits the node once with LANE = QUERY: lane q tests bit q of the mask, reads its
+// posting and accumulates ω·min(U m_μ, W m_ν) in a u64 register — no atomics, no per-query
+// probing.  Lane q then finalises the value of (q, doc).
 #include <algorithm>
 
 #include "ft_device.cuh"
 
 namespace {
 
+constexpr int QT_WARPS = 8;
+constexpr int QT_QC = 32;   // queries per chunk (= lanes)
+
+constexpr int QT_UCAP_S = 4096;   // distinct nodes staged in shared memory (else read from L2)
+constexpr int QT_PCAP_S = 8192;   // postings staged in shared memory (else read from L2)
+
+struct ChunkGeom {
+    int cap;        // hash capacity (pow2 > 1.25 umax)
+    int umax;       // max distinct nodes per chunk
+    int pmax;       // max postings per chunk
+    int ucap_s, pcap_s;
+    size_t off_keys, off_idx, off_mask, off_off, off_post, stride;
+};
+
+struct ChunkHdr {
+    uint32_t nU, nP, nq, pad;
+    uint32_t U[QT_QC];
+    uint32_t ok[QT_QC];
+    unsigned long long B[QT_QC];
+};
+
+ChunkGeom chunk_geom(const ft_dataset* ds, const QueryLayout& L) {
+    ChunkGeom g;
+    const int64_t per_q = std::min<int64_t>((int64_t)L.smax * std::max(1, ds->ix->d_star), ds->ix->M);
+    g.umax = (int)std::min<int64_t>(std::min<int64_t>((int64_t)QT_QC * per_q, ds->ix->M), 65535);
+    g.pmax = (int)((int64_t)QT_QC * per_q);
+    g.cap = fti_pow2_at_least(std::max(64, g.umax + g.umax / 4 + 1));
+    g.ucap_s = (std::min(g.umax, QT_UCAP_S) + 7) & ~7;   // multiples of 8 keep the u16 idx array 16-B aligned
+    g.pcap_s = (std::min(g.pmax, QT_PCAP_S) + 7) & ~7;
+    auto up = [](size_t x) { return (x + 15) / 16 * 16; };
+    size_t o = up(sizeof(ChunkHdr));
+    g.off_keys = o; o = up(o + 4ull * g.cap);
+    g.off_idx = o;  o = up(o + 2ull * g.cap);
+    g.off_mask = o; o = up(o + 4ull * g.umax);
+    g.off_off = o;  o = up(o + 4ull * g.umax);
+    g.off_post = o; o = up(o + 4ull * g.pmax);
+    g.stride = o;
+    return g;
+}
+
+__device__ __forceinline__ int probe_slot(const uint32_t* keys, uint32_t mask, uint32_t node) {
+    uint32_t h = fti_hash(node) & mask;
+    while (true) {
+        uint32_t k = keys[h];
+        if (k == node) return (int)h;
+        if (k == FTI_EMPTY) return -1;
+        h = (h + 1) & mask;
+    }
+}
+
+// one CTA per chunk: union hash of the chunk's query nodes with query masks and postings
+__global__ void __launch_bounds__(1024) k_qt_chunk(const uint8_t* __restrict__ qblock, QueryLayout L, int32_t nq,
+                                                   ChunkGeom g, uint8_t* __restrict__ chunks, uint32_t* err) {
+    extern __shared__ uint32_t smq[];
+    uint32_t* keys = smq;                         // cap
+    uint32_t* emask = keys + g.cap;               // umax
+    uint32_t* eoff = emask + g.umax;              // umax
+    uint16_t* idxs = (uint16_t*)(eoff + g.umax);  // cap
+    __shared__ int tmp[32];
+    __shared__ int s_overflow;
+    const int c = blockIdx.x;
+    const int q0 = c * QT_QC;
+    const int nqc = min(QT_QC, nq - q0);
+    uint8_t* out = chunks + (size_t)c * g.stride;
+    ChunkHdr* hdr = (ChunkHdr*)out;
+    const uint32_t cmask = (uint32_t)g.cap - 1;
+    for (int i = threadIdx.x; i < g.cap; i += blockDim.x) keys[i] = FTI_EMPTY;
+    if (threadIdx.x == 0) s_overflow = 0;
+    __syncthreads();
+    // flattened (query, slot) iteration over the chunk's node hashes
+    const int slots = L.nh_cap;
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        uint32_t h = fti_hash(e.x) & cmask;
+        while (true) {
+            uint32_t prev = atomicCAS(&keys[h], FTI_EMPTY, e.x);
+            if (prev == FTI_EMPTY || prev == e.x) break;
+            h = (h + 1) & cmask;
+        }
+    }
+    __syncthreads();
+    // dense ids of the distinct nodes (slot order)
+    int run = 0;
+    for (int b0 = 0; b0 < g.cap; b0 += blockDim.x) {
+        int i = b0 + threadIdx.x;
+        int f = (i < g.cap) ? (keys[i] != FTI_EMPTY) : 0;
+        int tot;
+        int r = run + fti_block_exclusive_sum(f, tmp, &tot);
+        if (f) {
+            if (r < g.umax) { idxs[i] = (uint16_t)r; emask[r] = 0; }
+            else s_overflow = 1;
+        }
+        run += tot;
+    }
+    const int nU = min(run, g.umax);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        int h = probe_slot(keys, cmask, e.x);
+        atomicOr(&emask[idxs[h]], 1u << ql);
+    }
+    __syncthreads();
+    int prun = 0;
+    for (int b0 = 0; b0 < nU; b0 += blockDim.x) {
+        int i = b0 + threadIdx.x;
+        int v = (i < nU) ? __popc(emask[i]) : 0;
+        int tot;
+        int r = prun + fti_block_exclusive_sum(v, tmp, &tot);
+        if (i < nU) eoff[i] = (uint32_t)r;
+        prun += tot;
+    }
+    const int nP = prun;
+    __syncthreads();
+    uint32_t* post = (uint32_t*)(out + g.off_post);
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        const uint32_t dep = (slot + L.off_nd)[s];
+        const int id = idxs[probe_slot(keys, cmask, e.x)];
+        const uint32_t mk = emask[id];
+        const uint32_t pos = eoff[id] + __popc(mk & ((1u << ql) - 1u));
+        if (pos < (uint32_t)g.pmax) post[pos] = (e.y & 0xFFFFu) | (dep << 16) | ((uint32_t)ql << 24);
+    }
+    // publish
+    uint32_t* gk = (uint32_t*)(out + g.off_keys);
+    uint16_t* gi = (uint16_t*)(out + g.off_idx);
+    uint32_t* gm = (uint32_t*)(out + g.off_mask);
+    uint32_t* go = (uint32_t*)(out + g.off_off);
+    for (int i = threadIdx.x; i < g.cap; i += blockDim.x) { gk[i] = keys[i]; gi[i] = idxs[i]; }
+    for (int i = threadIdx.x; i < nU; i += blockDim.x) { gm[i] = emask[i]; go[i] = eoff[i]; }
+    if (threadIdx.x < QT_QC) {
+        const int ql = threadIdx.x;
+        uint32_t U = 0, ok = 0;
+        unsigned long long B = 0;
+        if (ql < nqc) {
+            const QHeader* qh = (const QHeader*)(qblock + (size_t)(q0 + ql) * L.stride);
+            U = qh->U;
+            B = qh->B;
+            ok = (qh->err == 0 && qh->s > 0) ? 1u : 0u;
+        }
+        hdr->U[ql] = U;
+        hdr->ok[ql] = ok && !s_overflow;
+        hdr->B[ql] = B;
+    }
+    if (threadIdx.x == 0) {
+        hdr->nU = nU; hdr->nP = nP; hdr->nq = nqc;
+        if (s_overflow || nP > g.pmax) atomicOr(err, FTI_ERR_CAP);
+    }
+}
+
 struct QtArgs {
     const uint32_t* qt_off;
     const uint2* qt;
     const uint32_t* W;
     const unsigned long long* A;
-    const uint8_t* qblock;
-    QueryLayout L;
+    const uint8_t* chunks;
+    ChunkGeom g;
     int32_t nq;
     const int64_t* docs;
     int64_t n_docs;
@@ -33,92 +204,92 @@ struct QtArgs {
     double* out;
     int64_t out_ld;
     int d_star, l_root;
-    int QC;
-    int hcap;           // hash entries staged per query (max over the batch, = L.nh_cap)
     uint32_t* err;
 };
 
-constexpr int QT_WARPS = 8;
-
 __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
-    extern __shared__ unsigned long long sm[];
-    // layout: acc[QT_WARPS][QC] u64 | hash[QC][hcap] uint2 | depth[QC][hcap] u8
-    unsigned long long* acc = sm;
-    uint2* hs = (uint2*)(acc + QT_WARPS * a.QC);
-    uint8_t* hd = (uint8_t*)(hs + (size_t)a.QC * a.hcap);
-    __shared__ uint32_t s_mask[32], s_U[32], s_ok[32];
-    __shared__ unsigned long long s_B[32];
-
-    const int q0 = blockIdx.y * a.QC;
-    const int nqc = min(a.QC, a.nq - q0);
-    for (int t = threadIdx.x; t < nqc; t += blockDim.x) {
-        const QHeader* h = (const QHeader*)(a.qblock + (size_t)(q0 + t) * a.L.stride);
-        s_mask[t] = h->nh_mask;
-        s_U[t] = h->U;
-        s_B[t] = h->B;
-        s_ok[t] = (h->err == 0 && h->s > 0);
-    }
+    extern __shared__ uint32_t sm[];
+    __shared__ ChunkHdr sh;
+    const ChunkGeom& g = a.g;
+    uint32_t* keys = sm;                                  // cap
+    uint32_t* emask_s = keys + g.cap;                     // ucap_s
+    uint32_t* eoff_s = emask_s + g.ucap_s;                // ucap_s
+    uint32_t* post_s = eoff_s + g.ucap_s;                 // pcap_s
+    uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
+    const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
+    if (threadIdx.x == 0) sh = *(const ChunkHdr*)src;
     __syncthreads();
-    for (int t = 0; t < nqc; t++) {
-        const uint8_t* slot = a.qblock + (size_t)(q0 + t) * a.L.stride;
-        const uint2* src = (const uint2*)(slot + a.L.off_nh);
-        const uint8_t* srcd = slot + a.L.off_nd;
-        int n = (int)s_mask[t] + 1;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            hs[(size_t)t * a.hcap + i] = src[i];
-            hd[(size_t)t * a.hcap + i] = srcd[i];
-        }
+    const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
+    const uint32_t* gm = (const uint32_t*)(src + g.off_mask);
+    const uint32_t* go = (const uint32_t*)(src + g.off_off);
+    const uint32_t* gp = (const uint32_t*)(src + g.off_post);
+    // the hash lives in shared memory; masks/offsets/postings too when they fit, else in L2
+    const uint32_t* emask = nU <= g.ucap_s ? emask_s : gm;
+    const uint32_t* eoff = nU <= g.ucap_s ? eoff_s : go;
+    const uint32_t* post = nP <= g.pcap_s ? post_s : gp;
+    {
+        const uint4* k4 = (const uint4*)(src + g.off_keys);
+        for (int i = threadIdx.x; i < g.cap / 4; i += blockDim.x) ((uint4*)keys)[i] = k4[i];
+        const uint4* i4 = (const uint4*)(src + g.off_idx);
+        for (int i = threadIdx.x; i < g.cap / 8; i += blockDim.x) ((uint4*)idxs)[i] = i4[i];
+        if (nU <= g.ucap_s)
+            for (int i = threadIdx.x; i < nU; i += blockDim.x) { emask_s[i] = gm[i]; eoff_s[i] = go[i]; }
+        if (nP <= g.pcap_s)
+            for (int i = threadIdx.x; i < nP; i += blockDim.x) post_s[i] = gp[i];
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long* wacc = acc + warp * a.QC;
+    const uint32_t cmask = (uint32_t)g.cap - 1;
+    const uint32_t lt = (1u << lane) - 1u;
+    const unsigned long long Uq = sh.U[lane];
+    const unsigned long long Bq = sh.B[lane];
+    const bool okq = lane < nqc && sh.ok[lane];
+    const int q = blockIdx.y * QT_QC + lane;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
     for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
         const int64_t doc = a.docs ? a.docs[dp] : dp;
         if (doc < 0 || doc >= a.n) {
-            if (lane < nqc) a.out[(int64_t)(q0 + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+            if (lane < nqc) a.out[(int64_t)q * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
             if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
             continue;
         }
         const uint32_t r0 = a.qt_off[doc], r1 = a.qt_off[doc + 1];
-        const uint32_t W = a.W[doc];
-        for (int t = lane; t < nqc; t += 32) wacc[t] = 0ull;
-        __syncwarp();
-        for (uint32_t r = r0 + lane; r < r1; r += 32) {
-            const uint2 rec = a.qt[r];
-            const uint32_t hh = fti_hash(rec.x);
-            for (int t = 0; t < nqc; t++) {
-                const uint32_t mask = s_mask[t];
-                const uint2* tab = hs + (size_t)t * a.hcap;
-                uint32_t h = hh & mask;
-                while (true) {
-                    const uint2 e = tab[h];
-                    if (e.x == rec.x) {
-                        const unsigned long long um = (unsigned long long)s_U[t] * rec.y;
-                        const unsigned long long wm = (unsigned long long)W * e.y;
-                        const unsigned long long mn = um < wm ? um : wm;
-                        atomicAdd(&wacc[t], mn << (a.d_star - hd[(size_t)t * a.hcap + h]));
-                        break;
-                    }
-                    if (e.x == FTI_EMPTY) break;
-                    h = (h + 1) & mask;
+        const unsigned long long W = a.W[doc];
+        const unsigned long long A = a.A[doc];
+        unsigned long long acc = 0;
+        for (uint32_t rb = r0; rb < r1; rb += 32) {
+            const uint32_t r = rb + lane;
+            uint2 rec = make_uint2(FTI_EMPTY, 0);
+            int id = -1;
+            if (r < r1) {
+                rec = a.qt[r];
+                int h = probe_slot(keys, cmask, rec.x);
+                if (h >= 0) id = idxs[h];
+            }
+            unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
+            while (hm) {
+                const int l = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const int idl = __shfl_sync(0xffffffffu, id, l);
+                const uint32_t mmu = __shfl_sync(0xffffffffu, rec.y, l);
+                const uint32_t mk = emask[idl];
+                if ((mk >> lane) & 1u) {
+                    const uint32_t p = post[eoff[idl] + __popc(mk & lt)];
+                    const unsigned long long um = Uq * mmu;
+                    const unsigned long long wm = W * (p & 0xFFFFu);
+                    acc += (um < wm ? um : wm) << (a.d_star - (int)((p >> 16) & 63u));
                 }
             }
         }
-        __syncwarp();
         if (lane < nqc) {
             double val;
-            const unsigned long long U = s_U[lane];
-            const unsigned long long A = a.A[doc];
-            const unsigned long long B = s_B[lane];
-            const unsigned long long S2 = wacc[lane] << 1;
-            bool bad = !s_ok[lane];
-            bad |= __umul64hi(U, A) != 0ull || __umul64hi((unsigned long long)W, B) != 0ull;
-            const unsigned long long ua = U * A, wb = (unsigned long long)W * B;
+            bool bad = !okq;
+            bad |= __umul64hi(Uq, A) != 0ull || __umul64hi(W, Bq) != 0ull;
+            const unsigned long long ua = Uq * A, wb = W * Bq;
             const unsigned long long tot = ua + wb;
             bad |= tot < ua;
-            const unsigned long long num = tot - S2;
+            const unsigned long long num = tot - (acc << 1);
             if (!bad && num >= (1ull << 53)) {
                 bad = true;
                 atomicOr(a.err, FTI_ERR_OVERFLOW);
@@ -127,40 +298,47 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
                 val = __longlong_as_double(0x7ff8000000000000ll);
             } else {
                 const double scaled = scalbn((double)num, a.l_root - a.d_star);
-                val = __ddiv_rn(scaled, (double)(U * (unsigned long long)W));
+                val = __ddiv_rn(scaled, (double)(Uq * W));
             }
-            a.out[(int64_t)(q0 + lane) * a.out_ld + dp] = val;
+            a.out[(int64_t)q * a.out_ld + dp] = val;
         }
-        __syncwarp();
     }
 }
 
 }  // namespace
 
-cudaError_t fti_launch_qt(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
                           cudaStream_t st) {
     (void)docs_ld;   // the Quadtree stage always scores one doc list shared by the batch
     if (nq <= 0 || n_docs <= 0) return cudaSuccess;
+    const ChunkGeom g = chunk_geom(ds, L);
+    const int nchunks = (nq + QT_QC - 1) / QT_QC;
+    cudaError_t e = ds->s_chunk.reserve(g.stride * (size_t)nchunks);
+    if (e != cudaSuccess) return e;
+    size_t smem_c = 4ull * g.cap + 8ull * g.umax + 2ull * g.cap;
+    if (smem_c > 220 * 1024) return cudaErrorInvalidConfiguration;   // query batch too large for one chunk
+    e = cudaFuncSetAttribute(k_qt_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+    if (e != cudaSuccess) return e;
+    k_qt_chunk<<<nchunks, 1024, smem_c, st>>>(d_qblock, L, nq, g, ds->s_chunk.as<uint8_t>(), ds->err_dev);
     QtArgs a{};
     a.qt_off = ds->qt_off; a.qt = ds->qt; a.W = ds->W; a.A = ds->A;
-    a.qblock = d_qblock; a.L = L; a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
+    a.chunks = ds->s_chunk.as<uint8_t>(); a.g = g;
+    a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
-    a.hcap = L.nh_cap;
     a.err = ds->err_dev;
-    const size_t per_q = (size_t)a.hcap * 9 + QT_WARPS * 8;
-    int QC = (int)std::min<size_t>(16, std::max<size_t>(1, (96 * 1024) / per_q));
-    QC = std::min(QC, nq);
-    a.QC = QC;
-    const int qchunks = (nq + QC - 1) / QC;
-    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 63) / 64, (148 * 6 + qchunks - 1) / qchunks));
+    const size_t smem = 4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap;
+    e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int ctas_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_qt, QT_WARPS * 32, smem);
+    ctas_per_sm = std::max(1, ctas_per_sm);
+    const int64_t target = (int64_t)148 * ctas_per_sm * 4;
+    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + nchunks - 1) / nchunks));
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
-    size_t smem = (size_t)QT_WARPS * QC * 8 + (size_t)QC * a.hcap * 8 + (size_t)QC * a.hcap + 16;
-    cudaError_t e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_qt<<<dim3((unsigned)bx, (unsigned)qchunks), QT_WARPS * 32, smem, st>>>(a);
-    fti_count_launches(1);
+    k_qt<<<dim3((unsigned)bx, (unsigned)nchunks), QT_WARPS * 32, smem, st>>>(a);
+    fti_count_launches(2);
     return cudaGetLastError();
 }
