@@ -199,6 +199,7 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const size_t budget = (size_t)3 << 30;
     int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
+    FTI_RES(ds->s_centers, (size_t)qch * ix->d * 4);
     if (use_map) {
         FTI_RES(ds->s_map, (size_t)qch * ix->N * 4);
         FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);
@@ -222,7 +223,7 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
             StageTimer tm(ds, FTI_ST_DIST, st);
             FTI_CUDA(fti_launch_dist_table(ix, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
                                            use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
-                                           ds->s_table.as<float>(), ld, st));
+                                           ds->s_table.as<float>(), ld, ds->s_centers.as<float>(), st));
         }
         StageTimer tm(ds, FTI_ST_FT, st);
         FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,

@@ -143,7 +143,7 @@ struct ft_dataset {
     int64_t prof_n[FT_NUM_STAGES] = {0};
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_centers;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -170,7 +170,7 @@ cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint
                           cudaStream_t st);
 cudaError_t fti_launch_dist_table(const ft_index* ix, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap, float* d_table,
-                                  int32_t ld, cudaStream_t st);
+                                  int32_t ld, float* d_centers, cudaStream_t st);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, int32_t* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  cudaStream_t st);

@@ -206,6 +206,29 @@ def test_doc_subset_and_self_queries(ft):
             assert_ft_close([fl[qi, j]], [T.ft(*wl.doc(dd), ids_, w_)])
 
 
+def test_distance_table_accuracy(ft):
+    """FT(δ_x, δ_y) = ||x − y|| (one triple), so single-point docs/queries expose the tensor-core
+    (3xTF32, centred Gram form) distance table directly; compare with FP64 distances."""
+    wl = get_workload("reviews", n_docs=64, n_queries=2)
+    rng = np.random.default_rng(3)
+    N = wl.X.shape[0]
+    xs = rng.choice(N, 3000, replace=False).astype(np.int32)
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    ds = ft.Dataset(ix, np.arange(len(xs) + 1, dtype=np.int64), xs, np.ones(len(xs), np.uint32))
+    ys = rng.choice(N, 40, replace=False).astype(np.int32)
+    got = ds.flowtree(np.arange(len(ys) + 1, dtype=np.int64), ys, np.ones(len(ys), np.uint32))
+    Xd = wl.X.astype(np.float64)
+    ref = np.sqrt(((Xd[ys][:, None, :] - Xd[xs][None, :, :]) ** 2).sum(-1))
+    same = ys[:, None] == xs[None, :]
+    assert np.all(got[same] == 0.0)
+    rel = np.abs(got - ref)[~same] / ref[~same]
+    assert rel.max() < 2e-6, rel.max()
+    # the nearest pairs (within-cluster) are the hardest for the Gram form
+    rel = np.abs(got - ref) / np.where(same, 1.0, ref)
+    near = (ref < np.quantile(ref[~same], 0.01)) & ~same
+    assert rel[near].max() < 2e-6
+
+
 # ---------------------------------------------------------------------------------------------
 # k-NN
 # ---------------------------------------------------------------------------------------------
