@@ -17,6 +17,7 @@
 // The flow is priced with FP32 Euclidean distances (on the fly for d ≤ 32, else from the a5
 // table) and accumulated in FP64: FT = Σ η·dist / (W·U).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ft_device.cuh"
 
@@ -52,7 +53,11 @@ struct FtArgs {
     int small_d;
     int64_t n;
     uint32_t* err;
+    int use_bitmap;   // query vocab lookup by bitmap + rank (N small enough), else by hash
+    int nwords;       // bitmap words = ceil(N / 32)
 };
+
+constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
 
 constexpr int FT_WARPS = 8;
 
@@ -168,16 +173,78 @@ __device__ void nw_corner(const PairCtx& c, const uint16_t* a_list, int la, cons
     __syncwarp();
 }
 
+// The root northwest corner as a warp-parallel stable merge ("merge path") of the two cumulative
+// breakpoint lists SA (doc, vocab order) and SB (query, vocab order).  Walking the merged
+// sequence, the segment between consecutive breakpoints [m_t, m_{t+1}) belongs to the doc item a
+// and the query item b not yet consumed — exactly the triples of the sequential two-pointer
+// (zero-residual items give empty segments).  Each lane walks a contiguous range of the merged
+// sequence, found by one merge-path binary search; the flow is priced in FP32 per lane and
+// accumulated in FP64.  No residual update is needed after the root.
+template <bool EXPORT>
+__device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& cost) {
+    uint32_t carry = 0;
+    for (int p0 = 0; p0 < la; p0 += 32) {
+        int p = p0 + lane;
+        uint32_t v = p < la ? c.dres[p] : 0u;
+        uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < la) c.dcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    carry = 0;
+    for (int p0 = 0; p0 < lb; p0 += 32) {
+        int p = p0 + lane;
+        uint32_t v = p < lb ? c.qres[p] : 0u;
+        uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < lb) c.qcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const int L = la + lb;
+    const int per = (L + 31) >> 5;
+    const int t0 = min(L, lane * per), t1 = min(L, t0 + per);
+    float acc = 0.f;
+    if (t0 < t1) {
+        int lo = max(0, t0 - lb), hi = min(t0, la);
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            const int b = t0 - mid;
+            if (b == lb || c.dcum[mid - 1] <= c.qcum[b]) lo = mid; else hi = mid - 1;
+        }
+        int ai = lo, bi = t0 - lo;
+        const uint32_t ma = ai ? c.dcum[ai - 1] : 0u, mb = bi ? c.qcum[bi - 1] : 0u;
+        uint32_t m = ma > mb ? ma : mb;
+        for (int t = t0; t < t1; t++) {
+            const uint32_t va = ai < la ? c.dcum[ai] : 0xFFFFFFFFu;
+            const uint32_t vb = bi < lb ? c.qcum[bi] : 0xFFFFFFFFu;
+            const bool takeA = va <= vb;
+            const uint32_t nxt = takeA ? va : vb;
+            if (nxt > m && ai < la && bi < lb) {
+                const uint32_t eta = nxt - m;
+                const uint32_t x = c.dvoc[ai] & FTI_VOCAB_MASK;
+                const uint32_t y = c.qitem[bi].x & FTI_VOCAB_MASK;
+                if (x != y) acc = fmaf((float)eta, pair_dist(c, x, y, bi), acc);
+                emit<EXPORT>(*c.a, x, y, eta, 0u);
+            }
+            m = nxt;
+            if (takeA) ai++; else bi++;
+        }
+    }
+    cost += (double)acc;
+}
+
 template <bool EXPORT>
 __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int q = blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
     const QHeader* hdr = (const QHeader*)slot;
-    // shared layout: qitem[Sq] uint2 | vh[vh_cap] uint2 | Y[Sq*d] f32 (small d) | per-warp u32 arrays
+    // shared layout: qitem[Sq] uint2 | vocab lookup: bitmap[nw] + rank[nw] u32, or hash[vh_cap] uint2 |
+    //                Y[Sq*d] f32 (small d) | per-warp u32 arrays
     uint2* qitem = (uint2*)smraw;
-    uint2* vh = qitem + a.Sq;
-    float* Y = (float*)(vh + a.L.vh_cap);
+    uint32_t* bits = (uint32_t*)(qitem + a.Sq);
+    uint32_t* rank = bits + a.nwords;
+    uint2* vh = (uint2*)(qitem + a.Sq);
+    float* Y = a.use_bitmap ? (float*)(rank + a.nwords) : (float*)(vh + a.L.vh_cap);
     uint32_t* wbase = (uint32_t*)(Y + (a.small_d ? a.Sq * a.d : 0));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per_warp = 3 * a.Sd + 2 * a.Sq;
@@ -190,7 +257,28 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
     const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
     for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) qitem[i] = gitems[i];
-    for (int i = threadIdx.x; i <= (int)vh_mask; i += blockDim.x) vh[i] = gvh[i];
+    if (a.use_bitmap) {
+        // query vocab bitmap with per-word rank: rank(x) = index of x among the sorted query ids
+        for (int i = threadIdx.x; i < a.nwords; i += blockDim.x) bits[i] = 0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) {
+            const uint32_t x = gitems[i].x & FTI_VOCAB_MASK;
+            atomicOr(&bits[x >> 5], 1u << (x & 31));
+        }
+        __syncthreads();
+        __shared__ int tmp[32];
+        int run = 0;
+        for (int c0 = 0; c0 < a.nwords; c0 += blockDim.x) {
+            const int w = c0 + threadIdx.x;
+            const int v = w < a.nwords ? __popc(bits[w]) : 0;
+            int tot;
+            const int r = run + fti_block_exclusive_sum(v, tmp, &tot);
+            if (w < a.nwords) rank[w] = (uint32_t)r;
+            run += tot;
+        }
+    } else {
+        for (int i = threadIdx.x; i <= (int)vh_mask; i += blockDim.x) vh[i] = gvh[i];
+    }
     if (a.small_d) {
         for (int i = threadIdx.x; i < (int)sq * a.d; i += blockDim.x) {
             int j = i / a.d, t = i - j * a.d;
@@ -238,19 +326,25 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
             const uint32_t v = c.dvoc[i];
             if (v & FTI_FLAG_MULTI_LEAF) continue;
             const uint32_t x = v & FTI_VOCAB_MASK;
-            uint32_t h = fti_hash(x) & vh_mask;
-            while (true) {
-                const uint2 e = vh[h];
-                if (e.x == x) {
-                    const uint32_t dr = c.dres[i], qr = c.qres[e.y];
-                    const uint32_t eta = dr < qr ? dr : qr;
-                    c.dres[i] = dr - eta;
-                    c.qres[e.y] = qr - eta;
-                    if (EXPORT && eta) emit<EXPORT>(a, x, x, eta, (uint32_t)a.path[(int64_t)x * a.cols + a.leaf_depth[x]]);
-                    break;
+            int jq = -1;
+            if (a.use_bitmap) {
+                const uint32_t w = bits[x >> 5], bm = 1u << (x & 31);
+                if (w & bm) jq = (int)(rank[x >> 5] + __popc(w & (bm - 1u)));
+            } else {
+                uint32_t h = fti_hash(x) & vh_mask;
+                while (true) {
+                    const uint2 e = vh[h];
+                    if (e.x == x) { jq = (int)e.y; break; }
+                    if (e.x == FTI_EMPTY) break;
+                    h = (h + 1) & vh_mask;
                 }
-                if (e.x == FTI_EMPTY) break;
-                h = (h + 1) & vh_mask;
+            }
+            if (jq >= 0) {
+                const uint32_t dr = c.dres[i], qr = c.qres[jq];
+                const uint32_t eta = dr < qr ? dr : qr;
+                c.dres[i] = dr - eta;
+                c.qres[jq] = qr - eta;
+                if (EXPORT && eta) emit<EXPORT>(a, x, x, eta, (uint32_t)a.path[(int64_t)x * a.cols + a.leaf_depth[x]]);
             }
         }
         __syncwarp();
@@ -285,7 +379,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
             }
         }
         // ---- phase C: the root ----
-        nw_corner<EXPORT>(c, nullptr, s, nullptr, (int)sq, 0u, lane, cost);
+        root_merge<EXPORT>(c, s, (int)sq, lane, cost);
         cost = fti_warp_sum_f64(cost);
         if (lane == 0 && outp) *outp = cost / (double)((unsigned long long)W * U);
         __syncwarp();
@@ -319,7 +413,11 @@ cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint
     bx = std::max<int64_t>(bx, 1);
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
-    size_t smem = (size_t)a.Sq * 8 + (size_t)L.vh_cap * 8 + (a.small_d ? (size_t)a.Sq * a.d * 4 : 0) +
+    // FT_VOCAB_HASH=1 (test hook) forces the hash lookup used when N exceeds the bitmap limit
+    a.use_bitmap = (ix->N <= FT_BITMAP_MAX_N && !getenv("FT_VOCAB_HASH")) ? 1 : 0;
+    a.nwords = (int)((ix->N + 31) / 32);
+    const size_t lookup = a.use_bitmap ? (size_t)a.nwords * 8 : (size_t)L.vh_cap * 8;
+    size_t smem = (size_t)a.Sq * 8 + lookup + (a.small_d ? (size_t)a.Sq * a.d * 4 : 0) +
                   (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
     cudaError_t e;
     if (d_flow) {

@@ -206,6 +206,21 @@ def test_doc_subset_and_self_queries(ft):
             assert_ft_close([fl[qi, j]], [T.ft(*wl.doc(dd), ids_, w_)])
 
 
+def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
+    """The Flowtree kernel looks query vocab up by bitmap (N ≤ 2^19) or hash (larger N); both
+    must give identical values and flows (FT_VOCAB_HASH=1 forces the hash)."""
+    wl = get_workload("image", n_docs=300, n_queries=3)
+    ix, ds = _setup(ft, wl)
+    a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    f_a = ds.flow(*wl.query(1), 17)
+    monkeypatch.setenv("FT_VOCAB_HASH", "1")
+    b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    f_b = ds.flow(*wl.query(1), 17)
+    assert np.array_equal(a, b)
+    for key in f_a:
+        assert np.array_equal(f_a[key], f_b[key])
+
+
 def test_distance_table_accuracy(ft):
     """FT(δ_x, δ_y) = ||x − y|| (one triple), so single-point docs/queries expose the tensor-core
     (3xTF32, centred Gram form) distance table directly; compare with FP64 distances."""
