@@ -195,15 +195,17 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const int32_t ld = (S.L.smax + 3) & ~3;
     const bool use_map = d_docs != nullptr;
     const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
-    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? (size_t)ix->N * 4 + (size_t)rows_cap * 4 + 4 : 0);
+    // query chunks bounded by the worst-case table allocation (tables are written compactly)
+    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? (size_t)ix->N * 4 + (size_t)rows_cap * 4 + 12 : 0);
     const size_t budget = (size_t)3 << 30;
-    int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
+    const int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
     FTI_RES(ds->s_centers, (size_t)qch * ix->d * 4);
     if (use_map) {
         FTI_RES(ds->s_map, (size_t)qch * ix->N * 4);
         FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);
         FTI_RES(ds->s_rowcnt, (size_t)qch * 4);
+        FTI_RES(ds->s_rowbase, (size_t)qch * 8);
     }
     for (int32_t q0 = 0; q0 < nq; q0 += qch) {
         const int32_t nqc = std::min(qch, nq - q0);
@@ -216,14 +218,17 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         if (use_map) {
             StageTimer tm(ds, FTI_ST_VMAP, st);
             FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<int32_t>(),
-                                          ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap, st));
+                                          ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap,
+                                          ds->s_rowbase.as<int64_t>(), st));
             tab.map = ds->s_map.as<int32_t>();
+            tab.row_base = ds->s_rowbase.as<int64_t>();
         }
         {
             StageTimer tm(ds, FTI_ST_DIST, st);
-            FTI_CUDA(fti_launch_dist_table(ix, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
+            FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
                                            use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
-                                           ds->s_table.as<float>(), ld, ds->s_centers.as<float>(), st));
+                                           use_map ? ds->s_rowbase.as<int64_t>() : nullptr,
+                                           ds->s_table.as<float>(), ld, st));
         }
         StageTimer tm(ds, FTI_ST_FT, st);
         FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,

@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
     c.dcum = wsm + 2 * a.Sd;
     c.qres = wsm + 3 * a.Sd;
     c.qcum = wsm + 3 * a.Sd + a.Sq;
-    c.trow_base = a.tab.table ? a.tab.table + (int64_t)q * a.tab.rows_cap * a.tab.ld : nullptr;
+    c.trow_base = a.tab.table ? a.tab.table + (a.tab.row_base ? a.tab.row_base[q] : (int64_t)q * a.tab.rows_cap) *
+                                                  a.tab.ld
+                              : nullptr;
     c.map = a.tab.map ? a.tab.map + (int64_t)q * a.N : nullptr;
 
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
 
 }  // namespace
 
-cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
                           int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap, cudaStream_t st) {
     if (nq <= 0 || n_docs <= 0) return cudaSuccess;
@@ -417,8 +419,8 @@ cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint
     a.use_bitmap = (ix->N <= FT_BITMAP_MAX_N && !getenv("FT_VOCAB_HASH")) ? 1 : 0;
     a.nwords = (int)((ix->N + 31) / 32);
     const size_t lookup = a.use_bitmap ? (size_t)a.nwords * 8 : (size_t)L.vh_cap * 8;
-    size_t smem = (size_t)a.Sq * 8 + lookup + (a.small_d ? (size_t)a.Sq * a.d * 4 : 0) +
-                  (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
+    const size_t ysm = a.small_d ? (size_t)a.Sq * a.d * 4 : 0;
+    size_t smem = (size_t)a.Sq * 8 + lookup + ysm + (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
     cudaError_t e;
     if (d_flow) {
         e = cudaFuncSetAttribute(k_flowtree<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

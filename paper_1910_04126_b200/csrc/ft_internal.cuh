@@ -143,7 +143,7 @@ struct ft_dataset {
     int64_t prof_n[FT_NUM_STAGES] = {0};
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_centers;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_centers, s_rowbase, s_bsplit, s_ny, s_tiles;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -159,21 +159,22 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
                           cudaStream_t st);
 struct FtTable {
-    const float* table = nullptr;   // [nq][rows_cap][ld] or null (on-the-fly distances)
-    const int32_t* map = nullptr;   // [nq][N] vocab -> row, or null (row = vocab)
+    const float* table = nullptr;      // rows of ld floats, or null (on-the-fly distances)
+    const int32_t* map = nullptr;      // [nq][N] vocab -> row, or null (row = vocab)
+    const int64_t* row_base = nullptr; // [nq] first row of each query (compact), or null (q * rows_cap)
     int64_t rows_cap = 0;
     int32_t ld = 0;
 };
-cudaError_t fti_launch_ft(const ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab,
                           double* d_out, int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap,
                           cudaStream_t st);
-cudaError_t fti_launch_dist_table(const ft_index* ix, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
-                                  const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap, float* d_table,
-                                  int32_t ld, float* d_centers, cudaStream_t st);
+cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                                  const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
+                                  const int64_t* d_row_base, float* d_table, int32_t ld, cudaStream_t st);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, int32_t* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
-                                 cudaStream_t st);
+                                 int64_t* d_row_base, cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
                               cudaStream_t st);
