@@ -35,7 +35,9 @@ constexpr int KC = 16;                  // K elements per chunk (64 B per row)
 constexpr int RR = 4;                   // raw cp.async ring depth per producer thread
 constexpr int NCB = 256;                // query points per column block = max UMMA N
 constexpr int SBO = (KC / 4) * 128;     // bytes between 8-row core-matrix groups
-constexpr int NTHREADS = 9 * 32;        // 4 producer + 1 MMA + 4 epilogue warps
+constexpr int NPROD = 256;              // producer threads: 2 per row, 8 of the 16 K elements each
+constexpr int MMA_WARP = NPROD / 32;    // warp 8
+constexpr int NTHREADS = NPROD + 32 + 128;   // 8 producer + 1 MMA + 4 epilogue warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -138,8 +140,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
     uint8_t* stages = sm;
     float* raw = (float*)(sm + (size_t)a.R * stage_bytes);        // [RR][TM][KC]
-    float* nxs = raw + RR * TM * KC;                                // [2][TM]
-    uint64_t* bars = (uint64_t*)(nxs + 2 * TM);                     // full[R], empty[R], accf[2], acce[2], nxr[2]
+    float* nxs = raw + RR * TM * KC;                                // [2 buffers][2 halves][TM]
+    float* eny = nxs + 4 * TM;                                      // [NCB] ||y − c||^2 (epilogue)
+    uint32_t* eyid = (uint32_t*)(eny + NCB);                        // [NCB] query vocab ids (epilogue)
+    uint64_t* bars = (uint64_t*)(eyid + NCB);                       // full[R], empty[R], accf[2], acce[2], nxr[2]
     uint64_t* full = bars;
     uint64_t* empty = bars + a.R;
     uint64_t* accf = bars + 2 * a.R;
@@ -150,11 +154,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     const int64_t T = a.tile_base[a.nq];
     const uint32_t ncols = (uint32_t)fti_pow2_at_least(max(32, 2 * a.NPa));
     if (t == 0) {
-        for (int s = 0; s < a.R; s++) { mbar_init(&full[s], TM + 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], TM); mbar_init(&nxr[b], TM); }
+        for (int s = 0; s < a.R; s++) { mbar_init(&full[s], NPROD + 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], TM); mbar_init(&nxr[b], NPROD); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) {
+    if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(ncols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -164,9 +168,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
+    if (warp < MMA_WARP) {
         // ------------------------------------------------------------------ producers
+        // thread t handles row r = t % 128, K elements [8h, 8h + 8) of every 16-wide chunk, h = t / 128
         const bool vec = (a.d & 3) == 0;
+        const int r = t & (TM - 1), h = t >> 7;
         uint32_t it = 0;
         int k = 0;
         for (int64_t w = blockIdx.x; w < T; w += gridDim.x, k++) {
@@ -174,22 +180,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
             int64_t tile;
             decode_tile(a, w, q, tile);
             const int64_t nrows = a.rowcnt ? (int64_t)a.rowcnt[q] : a.rows_cap;
-            const int64_t row = tile * TM + t;
+            const int64_t row = tile * TM + r;
             const int32_t xid = row < nrows ? (a.rows ? a.rows[(int64_t)q * a.rows_cap + row] : (int32_t)row) : -1;
             const float* xr = a.X + (int64_t)(xid >= 0 ? xid : 0) * a.d;
             const float* cq = a.centers + (int64_t)q * a.d;
             const uint8_t* bq = a.bsplit + (size_t)q * a.nch * (2 * b_bytes);
-            float* myraw = raw + t * KC;
+            float* myraw = raw + r * KC + 8 * h;
             auto issue = [&](int cc) {
                 if (xid >= 0 && cc < a.nch) {
                     float* dst = myraw + (cc % RR) * TM * KC;
-                    const int k0 = cc * KC;
+                    const int k0 = cc * KC + 8 * h;
                     if (vec) {
 #pragma unroll
-                        for (int g = 0; g < KC / 4; g++)
+                        for (int g = 0; g < 2; g++)
                             if (k0 + 4 * g < a.d) cp_async16(dst + 4 * g, xr + k0 + 4 * g);
                     } else {
-                        for (int e = 0; e < KC; e++)
+                        for (int e = 0; e < 8; e++)
                             if (k0 + e < a.d) cp_async4(dst + e, xr + k0 + e);
                     }
                 }
@@ -214,31 +220,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                         : "memory");
                 }
                 const float* src = myraw + (cc % RR) * TM * KC;
-                const int k0 = cc * KC;
+                const int k0 = cc * KC + 8 * h;
 #pragma unroll
-                for (int g = 0; g < KC / 4; g++) {
+                for (int g = 0; g < 2; g++) {
                     const int kk = k0 + 4 * g;
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (xid >= 0) {
                         const float4 r4 = *(const float4*)(src + 4 * g);
-                        v.x = kk + 0 < a.d ? r4.x - cq[kk + 0] : 0.f;
-                        v.y = kk + 1 < a.d ? r4.y - cq[kk + 1] : 0.f;
-                        v.z = kk + 2 < a.d ? r4.z - cq[kk + 2] : 0.f;
-                        v.w = kk + 3 < a.d ? r4.w - cq[kk + 3] : 0.f;
+                        float4 c4;
+                        if (vec && kk < a.d) {
+                            c4 = __ldg((const float4*)(cq + kk));
+                        } else {
+                            c4.x = kk + 0 < a.d ? cq[kk + 0] : 0.f;
+                            c4.y = kk + 1 < a.d ? cq[kk + 1] : 0.f;
+                            c4.z = kk + 2 < a.d ? cq[kk + 2] : 0.f;
+                            c4.w = kk + 3 < a.d ? cq[kk + 3] : 0.f;
+                        }
+                        v.x = kk + 0 < a.d ? r4.x - c4.x : 0.f;
+                        v.y = kk + 1 < a.d ? r4.y - c4.y : 0.f;
+                        v.z = kk + 2 < a.d ? r4.z - c4.z : 0.f;
+                        v.w = kk + 3 < a.d ? r4.w - c4.w : 0.f;
                     }
                     nx = fmaf(v.x, v.x, nx); nx = fmaf(v.y, v.y, nx); nx = fmaf(v.z, v.z, nx); nx = fmaf(v.w, v.w, nx);
-                    split_store(st, st + a_bytes, t, g, v);
+                    split_store(st, st + a_bytes, r, 2 * h + g, v);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&full[s]);
             }
-            // hand ||x − c||^2 to the epilogue (after it released this buffer two tiles ago)
+            // hand the partial ||x − c||^2 to the epilogue (after it released this buffer two tiles ago)
             if (k >= 2) mbar_wait(&acce[b], ((k >> 1) - 1) & 1);
-            nxs[b * TM + t] = nx;
+            nxs[(b * 2 + h) * TM + r] = nx;
             mbar_arrive(&nxr[b]);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
-    } else if (warp == 4) {
+    } else if (warp == MMA_WARP) {
         // ------------------------------------------------------------------ MMA issuer
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.NPa >> 3) << 17) |
                                ((uint32_t)(TM >> 4) << 24);
@@ -286,7 +301,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
         // ------------------------------------------------------------------ epilogue
         const int quarter = warp & 3;                 // TMEM lanes 32*quarter .. +31
         const int r = quarter * 32 + lane;
-        int k = 0;
+        const int et = t - (NPROD + 32);              // 0..127 within the epilogue warps
+        int k = 0, cur_q = -1;
         for (int64_t w = blockIdx.x; w < T; w += gridDim.x, k++) {
             const int b = k & 1;
             int q;
@@ -294,16 +310,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
             decode_tile(a, w, q, tile);
             const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
             const QHeader* hdr = (const QHeader*)slot;
-            const uint2* qitems = (const uint2*)(slot + a.L.off_items);
             const int sq = hdr->err ? 0 : (int)hdr->s;
             const int nb = min(NCB, max(0, sq - a.cb * NCB));
+            if (q != cur_q) {   // stage the query's ids and norms once per query (named barrier: epilogue only)
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const uint2* qitems = (const uint2*)(slot + a.L.off_items);
+                for (int j = et; j < NCB; j += 128) {
+                    eyid[j] = j < nb ? (qitems[a.cb * NCB + j].x & FTI_VOCAB_MASK) : 0xFFFFFFFFu;
+                    eny[j] = j < a.NPa ? a.ny[(int64_t)q * a.NPa + j] : 0.f;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                cur_q = q;
+            }
             const int64_t nrows = a.rowcnt ? (int64_t)a.rowcnt[q] : a.rows_cap;
             const int64_t row = tile * TM + r;
             const int32_t xid = row < nrows ? (a.rows ? a.rows[(int64_t)q * a.rows_cap + row] : (int32_t)row) : -1;
             float* trow = a.table + ((a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) + row) * a.ld + a.cb * NCB;
-            const float* nyq = a.ny + (int64_t)q * a.NPa;
             mbar_wait(&nxr[b], (k >> 1) & 1);
-            const float nx = nxs[b * TM + r];
+            const float nx = nxs[(b * 2) * TM + r] + nxs[(b * 2 + 1) * TM + r];
             mbar_wait(&accf[b], (k >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.NPa);
@@ -314,15 +338,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                     : "r"(tb + (uint32_t)c0));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (xid >= 0) {
+                if (xid >= 0 && c0 < nb) {
+                    float o[8];
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
                         const int j = c0 + i;
-                        if (j < nb) {
-                            const float d2 = nx + nyq[j] - 2.f * __uint_as_float(v[i]);
-                            const uint32_t yid = qitems[a.cb * NCB + j].x & FTI_VOCAB_MASK;
-                            trow[j] = ((uint32_t)xid == yid) ? 0.f : sqrtf(fmaxf(d2, 0.f));
-                        }
+                        const float d2 = nx + eny[j] - 2.f * __uint_as_float(v[i]);
+                        o[i] = ((uint32_t)xid == eyid[j]) ? 0.f : sqrtf(fmaxf(d2, 0.f));
+                    }
+                    if (c0 + 8 <= nb && ((a.ld & 3) == 0)) {
+                        *(float4*)(trow + c0) = make_float4(o[0], o[1], o[2], o[3]);
+                        *(float4*)(trow + c0 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; i++)
+                            if (c0 + i < nb) trow[c0 + i] = o[i];
                     }
                 }
             }
@@ -333,7 +363,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+    if (warp == MMA_WARP)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
 }
 
 // per query: centroid c (FP32 mean of the support points), the centred query points of column
@@ -477,7 +508,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.tile_base = ds->s_tiles.as<int64_t>();
     k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, nullptr, ds->s_tiles.as<int64_t>());
     const size_t stage_bytes = 2 * (size_t)TM * KC * 4 + 2 * b_bytes;
-    const size_t fixed = (size_t)RR * TM * KC * 4 + 2 * TM * 4 + 16 * 8 * 2 + 64;
+    const size_t fixed = (size_t)RR * TM * KC * 4 + 4 * TM * 4 + 2 * NCB * 4 + 64;
     const int R = (int)std::max<size_t>(2, std::min<size_t>(8, (200 * 1024 - fixed) / stage_bytes));
     a.R = R;
     const size_t smem = (size_t)R * stage_bytes + fixed + (size_t)(2 * R + 6) * 8 + 16;
