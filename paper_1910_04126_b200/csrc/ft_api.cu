@@ -196,13 +196,14 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const bool use_map = d_docs != nullptr;
     const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
     // query chunks bounded by the worst-case table allocation (tables are written compactly)
-    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? (size_t)ix->N * 4 + (size_t)rows_cap * 4 + 12 : 0);
+    const size_t nwords = (size_t)(ix->N + 31) / 32;
+    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? nwords * 8 + (size_t)rows_cap * 4 + 12 : 0);
     const size_t budget = (size_t)3 << 30;
     const int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
     FTI_RES(ds->s_centers, (size_t)qch * ix->d * 4);
     if (use_map) {
-        FTI_RES(ds->s_map, (size_t)qch * ix->N * 4);
+        FTI_RES(ds->s_map, (size_t)qch * nwords * 8);
         FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);
         FTI_RES(ds->s_rowcnt, (size_t)qch * 4);
         FTI_RES(ds->s_rowbase, (size_t)qch * 8);
@@ -217,10 +218,10 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         tab.ld = ld;
         if (use_map) {
             StageTimer tm(ds, FTI_ST_VMAP, st);
-            FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<int32_t>(),
+            FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<uint2>(),
                                           ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap,
                                           ds->s_rowbase.as<int64_t>(), st));
-            tab.map = ds->s_map.as<int32_t>();
+            tab.map = ds->s_map.as<uint2>();
             tab.row_base = ds->s_rowbase.as<int64_t>();
         }
         {

@@ -420,37 +420,45 @@ __global__ void __launch_bounds__(256) k_dist_prep(DistArgs a, float* __restrict
     }
 }
 
-// warp per candidate doc: flag its vocab ids in the query's map
-__global__ void k_mark(const uint32_t* __restrict__ doc_off, const uint2* __restrict__ items,
-                       const int64_t* __restrict__ cand, int64_t cand_ld, int64_t n_cand, int64_t N,
-                       int32_t* __restrict__ map) {
-    const int q = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (c >= n_cand) return;
-    int64_t doc = cand[(int64_t)q * cand_ld + c];
-    if (doc < 0) return;
-    uint32_t i0 = doc_off[doc], i1 = doc_off[doc + 1];
-    int32_t* mq = map + (int64_t)q * N;
-    for (uint32_t i = i0 + lane; i < i1; i += 32) mq[items[i].x & FTI_VOCAB_MASK] = 1;
-}
-
-// one CTA per query: dense row ids in vocab order
-__global__ void __launch_bounds__(1024) k_compact(int64_t N, int32_t* __restrict__ map, int32_t* __restrict__ rows,
-                                                  int32_t* __restrict__ rowcnt, int64_t rows_cap) {
+// one CTA per query: the candidates' vocabulary as a shared-memory bitmap (shared atomics), then
+// per-word ranks (dense row ids in vocab order), the row list and the row count
+__global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc_off, const uint2* __restrict__ items,
+                                                const int64_t* __restrict__ cand, int64_t cand_ld, int64_t n_cand,
+                                                int64_t nwords, uint2* __restrict__ map, int32_t* __restrict__ rows,
+                                                int32_t* __restrict__ rowcnt, int64_t rows_cap) {
+    extern __shared__ uint32_t sbits[];
     __shared__ int tmp[32];
     const int q = blockIdx.x;
-    int32_t* mq = map + (int64_t)q * N;
+    for (int64_t i = threadIdx.x; i < nwords; i += blockDim.x) sbits[i] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t c = warp; c < n_cand; c += nw) {
+        const int64_t doc = cand[(int64_t)q * cand_ld + c];
+        if (doc < 0) continue;
+        const uint32_t i0 = doc_off[doc], i1 = doc_off[doc + 1];
+        for (uint32_t i = i0 + lane; i < i1; i += 32) {
+            const uint32_t x = items[i].x & FTI_VOCAB_MASK;
+            atomicOr(&sbits[x >> 5], 1u << (x & 31));
+        }
+    }
+    __syncthreads();
+    uint2* mq = map + (int64_t)q * nwords;
     int32_t* rq = rows + (int64_t)q * rows_cap;
     int run = 0;
-    for (int64_t c = 0; c < N; c += blockDim.x) {
-        int64_t v = c + threadIdx.x;
-        int f = (v < N) ? (mq[v] != 0) : 0;
+    for (int64_t c = 0; c < nwords; c += blockDim.x) {
+        const int64_t wi = c + threadIdx.x;
+        uint32_t bits = wi < nwords ? sbits[wi] : 0u;
         int tot;
-        int r = run + fti_block_exclusive_sum(f, tmp, &tot);
-        if (f) {
-            mq[v] = r;
-            if (r < rows_cap) rq[r] = (int32_t)v;
+        const int r = run + fti_block_exclusive_sum(__popc(bits), tmp, &tot);
+        if (wi < nwords) {
+            mq[wi] = make_uint2(bits, (uint32_t)r);
+            int rr = r;
+            while (bits) {
+                const int bpos = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (rr < rows_cap) rq[rr] = (int32_t)(wi * 32 + bpos);
+                rr++;
+            }
         }
         run += tot;
     }
@@ -525,18 +533,17 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
 }
 
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
-                                 int64_t n_cand, int32_t* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
+                                 int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  int64_t* d_row_base, cudaStream_t st) {
     if (nq <= 0) return cudaSuccess;
-    const int64_t N = ds->ix->N;
-    cudaError_t e = cudaMemsetAsync(d_map, 0, sizeof(int32_t) * N * nq, st);
+    const int64_t nwords = (ds->ix->N + 31) / 32;
+    const size_t smem = (size_t)nwords * 4;
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;   // N > 1.6M: not supported by the bitmap
+    cudaError_t e = cudaFuncSetAttribute(k_vocab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (n_cand > 0) {
-        dim3 g((unsigned)((n_cand * 32 + 255) / 256), (unsigned)nq);
-        k_mark<<<g, 256, 0, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, N, d_map);
-    }
-    k_compact<<<nq, 1024, 0, st>>>(N, d_map, d_rows, d_rowcnt, rows_cap);
+    k_vocab<<<nq, 1024, smem, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, nwords, d_map, d_rows, d_rowcnt,
+                                    rows_cap);
     k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, d_row_base, nullptr);
-    fti_count_launches(n_cand > 0 ? 3 : 2);
+    fti_count_launches(2);
     return cudaGetLastError();
 }

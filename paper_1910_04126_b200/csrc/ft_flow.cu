@@ -72,13 +72,17 @@ struct PairCtx {
     uint32_t* qres;
     uint32_t* qcum;
     const float* trow_base; // table for this query or null
-    const int32_t* map;     // vocab -> row map for this query or null
+    const uint2* map;       // candidate-vocabulary bitmap {bits, rank} per 32 ids, or null (row = vocab)
 };
 
 __device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_t y, int jq) {
     const FtArgs& a = *c.a;
     if (c.trow_base) {
-        int64_t row = c.map ? (int64_t)c.map[x] : (int64_t)x;
+        int64_t row = (int64_t)x;
+        if (c.map) {
+            const uint2 m = c.map[x >> 5];
+            row = (int64_t)(m.y + __popc(m.x & ((1u << (x & 31)) - 1u)));
+        }
         return c.trow_base[row * a.tab.ld + jq];
     }
     // on the fly, FP32 direct differences (the query row from shared memory when staged)
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
     c.trow_base = a.tab.table ? a.tab.table + (a.tab.row_base ? a.tab.row_base[q] : (int64_t)q * a.tab.rows_cap) *
                                                   a.tab.ld
                               : nullptr;
-    c.map = a.tab.map ? a.tab.map + (int64_t)q * a.N : nullptr;
+    c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
 
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);

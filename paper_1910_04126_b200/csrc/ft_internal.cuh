@@ -160,7 +160,7 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           cudaStream_t st);
 struct FtTable {
     const float* table = nullptr;      // rows of ld floats, or null (on-the-fly distances)
-    const int32_t* map = nullptr;      // [nq][N] vocab -> row, or null (row = vocab)
+    const uint2* map = nullptr;        // [nq][ceil(N/32)] {bits, rank}: row = rank + popc(bits below), or null
     const int64_t* row_base = nullptr; // [nq] first row of each query (compact), or null (q * rows_cap)
     int64_t rows_cap = 0;
     int32_t ld = 0;
@@ -173,7 +173,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
                                   const int64_t* d_row_base, float* d_table, int32_t ld, cudaStream_t st);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
-                                 int64_t n_cand, int32_t* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
+                                 int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  int64_t* d_row_base, cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
