@@ -58,8 +58,8 @@ ChunkGeom chunk_geom(const ft_dataset* ds, const QueryLayout& L) {
     size_t o = up(sizeof(ChunkHdr));
     g.off_keys = o; o = up(o + 4ull * g.cap);
     g.off_idx = o;  o = up(o + 2ull * g.cap);
-    g.off_mask = o; o = up(o + 4ull * g.umax);
-    g.off_off = o;  o = up(o + 4ull * g.umax);
+    g.off_mask = o; o = up(o + 8ull * g.umax);   // {query mask, posting offset} per distinct node
+    g.off_off = 0;
     g.off_post = o; o = up(o + 4ull * g.pmax);
     g.stride = o;
     return g;
@@ -165,10 +165,9 @@ __global__ void __launch_bounds__(1024) k_qt_chunk(const uint8_t* __restrict__ q
     // publish
     uint32_t* gk = (uint32_t*)(out + g.off_keys);
     uint16_t* gi = (uint16_t*)(out + g.off_idx);
-    uint32_t* gm = (uint32_t*)(out + g.off_mask);
-    uint32_t* go = (uint32_t*)(out + g.off_off);
+    uint2* ge = (uint2*)(out + g.off_mask);
     for (int i = threadIdx.x; i < g.cap; i += blockDim.x) { gk[i] = keys[i]; gi[i] = idxs[i]; }
-    for (int i = threadIdx.x; i < nU; i += blockDim.x) { gm[i] = emask[i]; go[i] = eoff[i]; }
+    for (int i = threadIdx.x; i < nU; i += blockDim.x) ge[i] = make_uint2(emask[i], eoff[i]);
     if (threadIdx.x < QT_QC) {
         const int ql = threadIdx.x;
         uint32_t U = 0, ok = 0;
@@ -212,20 +211,17 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
     __shared__ ChunkHdr sh;
     const ChunkGeom& g = a.g;
     uint32_t* keys = sm;                                  // cap
-    uint32_t* emask_s = keys + g.cap;                     // ucap_s
-    uint32_t* eoff_s = emask_s + g.ucap_s;                // ucap_s
-    uint32_t* post_s = eoff_s + g.ucap_s;                 // pcap_s
+    uint2* ent_s = (uint2*)(keys + g.cap);                // ucap_s {query mask, posting offset}
+    uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
     uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
     const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
     if (threadIdx.x == 0) sh = *(const ChunkHdr*)src;
     __syncthreads();
     const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
-    const uint32_t* gm = (const uint32_t*)(src + g.off_mask);
-    const uint32_t* go = (const uint32_t*)(src + g.off_off);
+    const uint2* ge = (const uint2*)(src + g.off_mask);
     const uint32_t* gp = (const uint32_t*)(src + g.off_post);
     // the hash lives in shared memory; masks/offsets/postings too when they fit, else in L2
-    const uint32_t* emask = nU <= g.ucap_s ? emask_s : gm;
-    const uint32_t* eoff = nU <= g.ucap_s ? eoff_s : go;
+    const uint2* ent = nU <= g.ucap_s ? ent_s : ge;
     const uint32_t* post = nP <= g.pcap_s ? post_s : gp;
     {
         const uint4* k4 = (const uint4*)(src + g.off_keys);
@@ -233,7 +229,7 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
         const uint4* i4 = (const uint4*)(src + g.off_idx);
         for (int i = threadIdx.x; i < g.cap / 8; i += blockDim.x) ((uint4*)idxs)[i] = i4[i];
         if (nU <= g.ucap_s)
-            for (int i = threadIdx.x; i < nU; i += blockDim.x) { emask_s[i] = gm[i]; eoff_s[i] = go[i]; }
+            for (int i = threadIdx.x; i < nU; i += blockDim.x) ent_s[i] = ge[i];
         if (nP <= g.pcap_s)
             for (int i = threadIdx.x; i < nP; i += blockDim.x) post_s[i] = gp[i];
     }
@@ -241,6 +237,7 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t U32 = sh.U[lane];
     const unsigned long long Uq = sh.U[lane];
     const unsigned long long Bq = sh.B[lane];
     const bool okq = lane < nqc && sh.ok[lane];
@@ -255,7 +252,8 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
             continue;
         }
         const uint32_t r0 = a.qt_off[doc], r1 = a.qt_off[doc + 1];
-        const unsigned long long W = a.W[doc];
+        const uint32_t W32 = a.W[doc];
+        const unsigned long long W = W32;
         const unsigned long long A = a.A[doc];
         unsigned long long acc = 0;
         for (uint32_t rb = r0; rb < r1; rb += 32) {
@@ -273,12 +271,13 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
                 hm &= hm - 1;
                 const int idl = __shfl_sync(0xffffffffu, id, l);
                 const uint32_t mmu = __shfl_sync(0xffffffffu, rec.y, l);
-                const uint32_t mk = emask[idl];
-                if ((mk >> lane) & 1u) {
-                    const uint32_t p = post[eoff[idl] + __popc(mk & lt)];
-                    const unsigned long long um = Uq * mmu;
-                    const unsigned long long wm = W * (p & 0xFFFFu);
-                    acc += (um < wm ? um : wm) << (a.d_star - (int)((p >> 16) & 63u));
+                const uint2 e = ent[idl];
+                if ((e.x >> lane) & 1u) {
+                    const uint32_t p = post[e.y + __popc(e.x & lt)];
+                    // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
+                    const uint32_t um = U32 * mmu;
+                    const uint32_t wm = W32 * (p & 0xFFFFu);
+                    acc += (unsigned long long)(um < wm ? um : wm) << (a.d_star - (int)((p >> 16) & 63u));
                 }
             }
         }
