@@ -156,13 +156,11 @@ def run_b200(args):
         dist = None
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
-    from paper_1910_04126_b200 import flowtree as ft, workloads
+    from paper_1910_04126_b200 import flowtree as ft, parallel, workloads
 
     Q = args.queries
     wl_all = workloads.make(CONFIG, n_queries=Q * world)
-    a, b = int(wl_all.q_off[rank * Q]), int(wl_all.q_off[(rank + 1) * Q])
-    q_off = (wl_all.q_off[rank * Q:(rank + 1) * Q + 1] - a).astype(np.int64)
-    q_ids_h, q_w_h = wl_all.q_ids[a:b], wl_all.q_w[a:b]
+    q_off, q_ids_h, q_w_h, _ = parallel.shard_queries(wl_all.q_off, wl_all.q_ids, wl_all.q_w, rank, world)
     wl = wl_all
     k, m = wl.k, wl.prefilter_m
 
@@ -209,30 +207,41 @@ def run_b200(args):
     ds.synchronize(stream)
     t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     stages = ft.profile_dict(ds.h)
+    units = {"dist_table": ft.ft_profile_units(ds.h, 4), "flowtree": ft.ft_profile_units(ds.h, 5)}
     ft.ft_profile_enable(ds.h, False)
-    if dist is not None:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
+    t_ms = parallel.max_over_ranks(t_ms, dist, dev)
     value = world * Q * args.steps / (t_ms / 1e3)
 
-    # ---- dominant kernel of the step and its live roofline ----
+    # ---- live roofline of the step's kernels; `roofline` is the dominant one (largest device time) ----
+    # algorithmic bytes (SURVEY §8(d) and DESIGN.md §7): Quadtree 8 B per doc tree node + 16 B per doc
+    # per query scan; distance table rows·(4d + 4 s_q); Flowtree pairs·(8 s_doc + 16) — the last two
+    # counted on the device by the library during the timed region.
     peak, peak_src = measured_peaks()
     n_qt = ds.n_qt
-    qt_bytes = Q * (8 * n_qt + 16 * ds.n)        # 8 B per doc tree node + 16 B per doc, per query scan
-    dom = max(stages.items(), key=lambda kv: kv[1][0])
-    qt_ms, qt_n = stages["quadtree"]
-    qt_avg = qt_ms / max(qt_n, 1)
-    achieved = qt_bytes / (qt_avg / 1e3) / 1e9
-    traffic = None
+    qt_bytes = Q * (8 * n_qt + 16 * ds.n)
+    alg_bytes = {"quadtree": qt_bytes * stages["quadtree"][1], "dist_table": units["dist_table"],
+                 "flowtree": units["flowtree"]}
+    kern = {"quadtree": "k_qt (Quadtree estimate, a3)", "dist_table": "k_dist_tc (tcgen05 distance table, a5)",
+            "flowtree": "k_flowtree (Flowtree estimate, a6)"}
+    traffic_all = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("k_qt_dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "kernel": "k_qt (Quadtree estimate, a3)", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": qt_bytes, "launch_ms": qt_avg, "peak_source": peak_src,
-                "dominant_stage": dom[0]}
+            traffic_all = json.load(f)
+    rooflines = {}
+    for stg, b in alg_bytes.items():
+        ms, n = stages[stg]
+        if n == 0 or ms <= 0 or b <= 0:
+            continue
+        ach = b / (ms / 1e3) / 1e9
+        rooflines[stg] = {"bound": "hbm", "kernel": kern[stg], "achieved": ach, "peak": peak, "unit": "GB/s",
+                          "frac": ach / peak, "traffic": traffic_all.get(f"{stg}_dram_bytes_per_launch"),
+                          "algorithmic_bytes_per_launch": b / n, "launch_ms": ms / n, "launches": n,
+                          "share_of_step": ms / max(t_ms, 1e-9), "peak_source": peak_src}
+    if "quadtree" in rooflines and rooflines["quadtree"]["traffic"] is None:
+        rooflines["quadtree"]["traffic"] = traffic_all.get("k_qt_dram_bytes_per_launch")
+    dom = max(rooflines, key=lambda s: stages[s][0])
+    roofline = dict(rooflines[dom], dominant_stage=dom)
 
     # ---- kernel-level numbers over all n docs (separately timed; not part of the step) ----
     kernels = {}
@@ -289,10 +298,7 @@ def run_b200(args):
         e1.synchronize()
         e_ms += e0.elapsed_time(e1)
     barrier_sync()
-    if dist is not None:
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
+    e_ms = parallel.max_over_ranks(e_ms, dist, dev)
     h2d = 8 * (Q + 1) + 4 * len(q_ids_h) + 4 * len(q_w_h)
     d2h = Q * k * (8 + 8)
     e2e = {"value": world * Q * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
@@ -321,7 +327,7 @@ def run_b200(args):
                        "qt_records": int(n_qt), "nnz": int(ds.nnz)},
             "ft_estimates_per_s": kernels.get("flowtree_all_docs", {}).get("pairs_per_s"),
             "qt_estimates_per_s": kernels.get("quadtree_all_docs", {}).get("pairs_per_s"),
-            "roofline": roofline, "kernels": kernels,
+            "roofline": roofline, "rooflines_by_stage": rooflines, "kernels": kernels,
             "stages_ms_per_step": {s: v[0] / args.steps for s, v in stages.items()},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
             "build_s": build_s, "load_s": load_s,

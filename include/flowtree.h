@@ -128,6 +128,10 @@ ft_status ft_synchronize(const ft_dataset* ds, void* stream);
 ft_status ft_profile_enable(ft_dataset* ds, int32_t enable);
 ft_status ft_profile_reset(ft_dataset* ds);
 ft_status ft_profile_read(ft_dataset* ds, int32_t stage, double* total_ms, int64_t* launches);
+/* Algorithmic bytes the kernels of a stage moved since the last reset (SURVEY §8(d) units),
+ * counted on the device while profiling is enabled: stage 4 (distance table) Σ rows·(4d + 4 s_q),
+ * stage 5 (Flowtree) Σ pairs·(8 s_doc + 16).  Synchronises the device.                        */
+ft_status ft_profile_units(ft_dataset* ds, int32_t stage, uint64_t* bytes);
 const char* ft_profile_stage_name(int32_t stage);
 uint64_t ft_launch_count(void);
 

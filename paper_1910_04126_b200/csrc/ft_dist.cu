@@ -466,18 +466,26 @@ __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc
 }
 
 // compact table placement (exclusive prefix of the row counts) and the work list of 128-row tiles
+// (with `units`: adds the stage's algorithmic bytes Σ_q rows_q · (4 d + 4 s_q) for the profiler)
 __global__ void k_row_base(const int32_t* __restrict__ rowcnt, int64_t rows_cap, int nq,
-                           int64_t* __restrict__ row_base, int64_t* __restrict__ tile_base) {
+                           int64_t* __restrict__ row_base, int64_t* __restrict__ tile_base,
+                           const uint8_t* qblock, QueryLayout L, int d, unsigned long long* units) {
     if (threadIdx.x == 0) {
         int64_t acc = 0, tacc = 0;
+        unsigned long long bytes = 0;
         for (int q = 0; q < nq; q++) {
             const int64_t r = rowcnt ? (int64_t)rowcnt[q] : rows_cap;
             if (row_base) row_base[q] = acc;
             if (tile_base) tile_base[q] = tacc;
             acc += r;
             tacc += (r + TM - 1) / TM;
+            if (units) {
+                const QHeader* h = (const QHeader*)(qblock + (size_t)q * L.stride);
+                bytes += (unsigned long long)r * (4ull * d + 4ull * (h->err ? 0u : h->s));
+            }
         }
         if (tile_base) tile_base[nq] = tacc;
+        if (units) atomicAdd(units, bytes);
     }
 }
 
@@ -514,7 +522,8 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.bsplit = ds->s_bsplit.as<uint8_t>();
     a.ny = ds->s_ny.as<float>();
     a.tile_base = ds->s_tiles.as<int64_t>();
-    k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, nullptr, ds->s_tiles.as<int64_t>());
+    k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, nullptr, ds->s_tiles.as<int64_t>(), d_qblock, L, ix->d,
+                                 ds->units_ptr(FTI_ST_DIST));
     const size_t stage_bytes = 2 * (size_t)TM * KC * 4 + 2 * b_bytes;
     const size_t fixed = (size_t)RR * TM * KC * 4 + 4 * TM * 4 + 2 * NCB * 4 + 64;
     const int R = (int)std::max<size_t>(2, std::min<size_t>(8, (200 * 1024 - fixed) / stage_bytes));
@@ -543,7 +552,7 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
     if (e != cudaSuccess) return e;
     k_vocab<<<nq, 1024, smem, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, nwords, d_map, d_rows, d_rowcnt,
                                     rows_cap);
-    k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, d_row_base, nullptr);
+    k_row_base<<<1, 32, 0, st>>>(d_rowcnt, rows_cap, nq, d_row_base, nullptr, nullptr, QueryLayout{}, 0, nullptr);
     fti_count_launches(2);
     return cudaGetLastError();
 }

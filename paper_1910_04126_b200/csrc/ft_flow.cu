@@ -55,6 +55,7 @@ struct FtArgs {
     uint32_t* err;
     int use_bitmap;   // query vocab lookup by bitmap + rank (N small enough), else by hash
     int nwords;       // bitmap words = ceil(N / 32)
+    unsigned long long* units;   // profiler: Σ pairs (8 s_doc + 16) algorithmic bytes, or null
 };
 
 constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
                               : nullptr;
     c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
 
+    unsigned long long ubytes = 0;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
     for (int64_t dp = d0 + warp; dp < d1; dp += FT_WARPS) {
@@ -387,9 +389,11 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
         // ---- phase C: the root ----
         root_merge<EXPORT>(c, s, (int)sq, lane, cost);
         cost = fti_warp_sum_f64(cost);
+        ubytes += 8ull * (unsigned long long)s + 16ull;
         if (lane == 0 && outp) *outp = cost / (double)((unsigned long long)W * U);
         __syncwarp();
     }
+    if (a.units && lane == 0 && ubytes) atomicAdd(a.units, ubytes);
 }
 
 }  // namespace
@@ -413,6 +417,7 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     a.Sq = L.smax;
     a.n = ds->n;
     a.err = ds->err_dev;
+    a.units = d_flow ? nullptr : ds->units_ptr(FTI_ST_FT);
     a.small_d = (tab.table == nullptr && ix->d <= FTI_SMALL_D) ? 1 : 0;
     int64_t per_cta_target = std::max<int64_t>(FT_WARPS, (n_docs * nq + 148 * 16 - 1) / (148 * 16));
     int64_t bx = std::max<int64_t>(1, (n_docs + per_cta_target - 1) / per_cta_target);

@@ -141,6 +141,8 @@ struct ft_dataset {
     std::vector<cudaEvent_t> prof_pool;
     double prof_ms[FT_NUM_STAGES] = {0};
     int64_t prof_n[FT_NUM_STAGES] = {0};
+    unsigned long long* prof_units = nullptr;   // device [FT_NUM_STAGES] algorithmic bytes per stage
+    unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
     DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_centers, s_rowbase, s_bsplit, s_ny, s_tiles;

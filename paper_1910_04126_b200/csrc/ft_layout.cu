@@ -354,6 +354,8 @@ extern "C" ft_status ft_load_dataset(const ft_index* ix, const int64_t* doc_off,
     cudaStreamDestroy(st);
     FTI_CUDA(cudaMalloc(&ds->err_dev, sizeof(uint32_t) * 4));
     FTI_CUDA(cudaMemset(ds->err_dev, 0, sizeof(uint32_t) * 4));
+    FTI_CUDA(cudaMalloc(&ds->prof_units, sizeof(unsigned long long) * FT_NUM_STAGES));
+    FTI_CUDA(cudaMemset(ds->prof_units, 0, sizeof(unsigned long long) * FT_NUM_STAGES));
     *out = ds;
     return FT_OK;
 }
@@ -373,6 +375,7 @@ extern "C" void ft_dataset_free(ft_dataset* ds) {
     cudaFree(ds->doc_off); cudaFree(ds->items); cudaFree(ds->W); cudaFree(ds->mn_off); cudaFree(ds->mnodes);
     cudaFree(ds->mlists); cudaFree(ds->qt_off); cudaFree(ds->qt); cudaFree(ds->A);
     if (ds->err_dev) cudaFree(ds->err_dev);
+    if (ds->prof_units) cudaFree(ds->prof_units);
     DevBuf* bufs[] = {&ds->s_qoff, &ds->s_qids, &ds->s_qw, &ds->s_qblock, &ds->s_docs, &ds->s_vals, &ds->s_vals2,
                       &ds->s_cand, &ds->s_outid, &ds->s_outval, &ds->s_map, &ds->s_rows, &ds->s_rowcnt,
                       &ds->s_table, &ds->s_flow, &ds->s_flowcnt, &ds->s_vlist, &ds->s_chunk, &ds->s_centers, &ds->s_rowbase, &ds->s_bsplit, &ds->s_ny, &ds->s_tiles};

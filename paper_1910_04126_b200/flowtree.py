@@ -26,8 +26,8 @@ EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft
             "ft_index_sigma", "ft_index_nodes", "ft_load_dataset", "ft_dataset_info",
             "ft_quadtree_estimate", "ft_flowtree_estimate", "ft_flowtree_flow", "ft_knn",
             "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error",
-            "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_stage_name",
-            "ft_launch_count"]
+            "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_units",
+            "ft_profile_stage_name", "ft_launch_count"]
 FT_NUM_STAGES = 7
 
 
@@ -65,6 +65,7 @@ def _load_lib():
         "ft_profile_enable": (st, [P, i32]),
         "ft_profile_reset": (st, [P]),
         "ft_profile_read": (st, [P, i32, P, P]),
+        "ft_profile_units": (st, [P, i32, P]),
         "ft_profile_stage_name": (ctypes.c_char_p, [i32]),
         "ft_launch_count": (u64, []),
     }
@@ -265,6 +266,13 @@ def ft_profile_read(ds, stage: int):
     ms = ctypes.c_double(); n = ctypes.c_int64()
     _check(_lib.ft_profile_read(ds, stage, ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def ft_profile_units(ds, stage: int) -> int:
+    """Algorithmic bytes counted on the device for a stage since the last reset."""
+    v = ctypes.c_uint64()
+    _check(_lib.ft_profile_units(ds, stage, ctypes.byref(v)))
+    return int(v.value)
 
 
 def ft_profile_stage_name(stage: int) -> str:

@@ -1,0 +1,25 @@
+#!/bin/bash
+# Run on the GPU box (gpurun): launch list of the bench command + ncu --set full of the top kernels.
+# Each ncu command runs only after the same command line exited 0 without ncu.
+set -u
+mkdir -p gpurun_out
+B="python bench.py --steps 2 --warmup 3 --no-kernels --no-cpu-baseline"
+$B > gpurun_out/bench_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B \
+  > gpurun_out/ncu_launches.log 2>&1
+echo "launch list rc=$?"
+Q="python tools/kprof.py qt --queries 1000 --reps 1"
+$Q > gpurun_out/kp_qt.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_qt$" -c 1 -o gpurun_out/prof_qt $Q \
+  > gpurun_out/ncu_qt.log 2>&1
+echo "qt rc=$?"
+K="python tools/kprof.py knn --queries 200 --reps 1"
+$K > gpurun_out/kp_knn.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_dist_tc|k_flowtree|k_select|k_vocab" -c 6 \
+  -o gpurun_out/prof_knn $K > gpurun_out/ncu_knn.log 2>&1
+echo "knn rc=$?"
+F="python tools/kprof.py ft --queries 16 --reps 1"
+$F > gpurun_out/kp_ft.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_flowtree" -c 1 -o gpurun_out/prof_ft $F \
+  > gpurun_out/ncu_ft.log 2>&1
+echo "ft rc=$?"
