@@ -1,0 +1,61 @@
+"""Run ft_knn (BASELINE config's k / prefilter) on every config with device-resident queries and
+report the device time per query batch, plus a sampled oracle check of the Quadtree and Flowtree
+values at full size.  python tools/config_sweep.py [names...]"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+from paper_1910_04126_b200 import flowtree as ft, workloads  # noqa: E402
+
+names = sys.argv[1:] or ["tiny", "text", "reviews", "image", "stress"]
+dev = torch.device("cuda:0")
+for name in names:
+    t0 = time.perf_counter()
+    wl = workloads.make(name)
+    tg = time.perf_counter() - t0
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    qi = torch.from_numpy(wl.q_ids).to(dev)
+    qw = torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32)
+    oid = torch.empty((wl.nq, wl.k), dtype=torch.int64, device=dev)
+    ov = torch.empty((wl.nq, wl.k), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream()
+    ds.knn(wl.q_off, qi, qw, wl.k, wl.prefilter_m, out_ids=oid, out_val=ov, stream=st)
+    ds.synchronize(st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    ds.knn(wl.q_off, qi, qw, wl.k, wl.prefilter_m, out_ids=oid, out_val=ov, stream=st)
+    e1.record(st)
+    ds.synchronize(st)
+    ms = e0.elapsed_time(e1)
+    # sampled oracle check at full size (QT bit-exact, FT within 1e-5)
+    T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    rng = np.random.default_rng(5)
+    qs = rng.integers(0, wl.nq, 4)
+    ds_ = rng.integers(0, wl.n, 32).astype(np.int64)
+    sub = wl.subset_queries(wl.nq)
+    qt = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w, docs=ds_)
+    fv = ds.flowtree(wl.q_off[: int(qs.max()) + 2], wl.q_ids, wl.q_w, docs=ds_)
+    bad_qt = bad_ft = 0
+    for q in qs:
+        b, bw = wl.query(q)
+        for j, d in enumerate(ds_):
+            a, aw = wl.doc(d)
+            if qt[q, j] != T.qt(a, aw, b, bw)[1]:
+                bad_qt += 1
+            ref = T.ft(a, aw, b, bw)
+            if abs(fv[q, j] - ref) > 1e-5 * abs(ref) or (ref == 0) != (fv[q, j] == 0):
+                bad_ft += 1
+    print(json.dumps({"config": name, "n": wl.n, "nq": wl.nq, "N": int(wl.X.shape[0]), "d": int(wl.X.shape[1]),
+                      "d_star": ix.d_star, "nodes": ix.n_nodes, "k": wl.k, "prefilter_m": wl.prefilter_m,
+                      "knn_ms": ms, "queries_per_s": wl.nq / (ms / 1e3), "gen_s": round(tg, 1),
+                      "sampled_pairs": int(len(qs) * len(ds_)), "qt_mismatch": bad_qt, "ft_mismatch": bad_ft}),
+          flush=True)
+    ds.close()
+    ix.close()
