@@ -201,7 +201,6 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const size_t budget = (size_t)3 << 30;
     const int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
-    FTI_RES(ds->s_centers, (size_t)qch * ix->d * 4);
     if (use_map) {
         FTI_RES(ds->s_map, (size_t)qch * nwords * 8);
         FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);

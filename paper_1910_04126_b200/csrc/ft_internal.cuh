@@ -82,6 +82,11 @@ struct ft_index {
     uint8_t* node_depth = nullptr;    // [M]
     int32_t* node_count = nullptr;    // [M] ground points in the cell
     uint32_t* vflags = nullptr;       // [N] FTI_FLAG_* per ground point
+    // distance-table operand (built on first use, ft_dist.cu): the points translated by their FP64
+    // mean, FP32, rows padded to dpad (a multiple of 32) and one extra all-zero row N; their norms
+    float* Xc = nullptr;              // [(N+1)*dpad]
+    float* xnorm = nullptr;           // [N+1] ||x − mean||^2
+    int32_t dpad = 0;
     int device = 0;
 };
 
@@ -145,7 +150,7 @@ struct ft_dataset {
     unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_centers, s_rowbase, s_bsplit, s_ny, s_tiles;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow;
 };
 
 // ---------------------------------------------------------------------------------------------
