@@ -25,7 +25,7 @@
 
 namespace {
 
-constexpr int QT_WARPS = 8;
+constexpr int QT_WARPS = 32;   // 1024 threads share one staged chunk structure
 constexpr int QT_QC = 32;   // queries per chunk (= lanes)
 
 constexpr int QT_UCAP_S = 4096;   // distinct nodes staged in shared memory (else read from L2)
@@ -206,34 +206,13 @@ struct QtArgs {
     uint32_t* err;
 };
 
-__global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
-    extern __shared__ uint32_t sm[];
-    __shared__ ChunkHdr sh;
+// the doc scan of one CTA; SMEM: the masks/offsets and postings are in shared memory (the common
+// case), so every lookup is an LDS rather than a generic load
+template <bool SMEM>
+__device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restrict__ keys,
+                                        const uint2* __restrict__ ent, const uint32_t* __restrict__ post,
+                                        const uint16_t* __restrict__ idxs, const ChunkHdr& sh, int nqc) {
     const ChunkGeom& g = a.g;
-    uint32_t* keys = sm;                                  // cap
-    uint2* ent_s = (uint2*)(keys + g.cap);                // ucap_s {query mask, posting offset}
-    uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
-    uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
-    const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
-    if (threadIdx.x == 0) sh = *(const ChunkHdr*)src;
-    __syncthreads();
-    const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
-    const uint2* ge = (const uint2*)(src + g.off_mask);
-    const uint32_t* gp = (const uint32_t*)(src + g.off_post);
-    // the hash lives in shared memory; masks/offsets/postings too when they fit, else in L2
-    const uint2* ent = nU <= g.ucap_s ? ent_s : ge;
-    const uint32_t* post = nP <= g.pcap_s ? post_s : gp;
-    {
-        const uint4* k4 = (const uint4*)(src + g.off_keys);
-        for (int i = threadIdx.x; i < g.cap / 4; i += blockDim.x) ((uint4*)keys)[i] = k4[i];
-        const uint4* i4 = (const uint4*)(src + g.off_idx);
-        for (int i = threadIdx.x; i < g.cap / 8; i += blockDim.x) ((uint4*)idxs)[i] = i4[i];
-        if (nU <= g.ucap_s)
-            for (int i = threadIdx.x; i < nU; i += blockDim.x) ent_s[i] = ge[i];
-        if (nP <= g.pcap_s)
-            for (int i = threadIdx.x; i < nP; i += blockDim.x) post_s[i] = gp[i];
-    }
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
@@ -302,6 +281,40 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
             a.out[(int64_t)q * a.out_ld + dp] = val;
         }
     }
+}
+
+__global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
+    extern __shared__ uint32_t sm[];
+    __shared__ ChunkHdr sh;
+    const ChunkGeom& g = a.g;
+    uint32_t* keys = sm;                                  // cap
+    uint2* ent_s = (uint2*)(keys + g.cap);                // ucap_s {query mask, posting offset}
+    uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
+    uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
+    const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
+    if (threadIdx.x == 0) sh = *(const ChunkHdr*)src;
+    __syncthreads();
+    const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
+    const uint2* ge = (const uint2*)(src + g.off_mask);
+    const uint32_t* gp = (const uint32_t*)(src + g.off_post);
+    // the hash lives in shared memory; masks/offsets/postings too when they fit, else in L2
+    const uint2* ent = nU <= g.ucap_s ? ent_s : ge;
+    const uint32_t* post = nP <= g.pcap_s ? post_s : gp;
+    {
+        const uint4* k4 = (const uint4*)(src + g.off_keys);
+        for (int i = threadIdx.x; i < g.cap / 4; i += blockDim.x) ((uint4*)keys)[i] = k4[i];
+        const uint4* i4 = (const uint4*)(src + g.off_idx);
+        for (int i = threadIdx.x; i < g.cap / 8; i += blockDim.x) ((uint4*)idxs)[i] = i4[i];
+        if (nU <= g.ucap_s)
+            for (int i = threadIdx.x; i < nU; i += blockDim.x) ent_s[i] = ge[i];
+        if (nP <= g.pcap_s)
+            for (int i = threadIdx.x; i < nP; i += blockDim.x) post_s[i] = gp[i];
+    }
+    __syncthreads();
+    if (nU <= g.ucap_s && nP <= g.pcap_s)
+        qt_scan<true>(a, keys, ent_s, post_s, idxs, sh, nqc);
+    else
+        qt_scan<false>(a, keys, ent, post, idxs, sh, nqc);
 }
 
 }  // namespace
