@@ -369,12 +369,15 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
         d_val = ds->s_outval.as<double>();
     }
     const int64_t n = ds->n;
+    FTI_RES(ds->s_sel, sizeof(int) * ((size_t)nq + 1));
+    int* sel_scratch = ds->s_sel.as<int>();
     if (exhaustive) {
         FTI_RES(ds->s_vals, sizeof(double) * nq * n);
         rc = flowtree_stage(ds, S, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st);
         if (rc) return rc;
         StageTimer tm(ds, FTI_ST_SELK, st);
-        FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, k, d_ids, d_val, k, st));
+        FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, k, d_ids, d_val, k, sel_scratch,
+                                   st));
     } else {
         const int64_t m = prefilter_m;
         FTI_RES(ds->s_vals, sizeof(double) * nq * n);
@@ -387,13 +390,13 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
         {
             StageTimer tm(ds, FTI_ST_SELM, st);
             FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m,
-                                       ds->s_cand.as<int64_t>(), ds->s_vals2.as<double>(), m, st));
+                                       ds->s_cand.as<int64_t>(), ds->s_vals2.as<double>(), m, sel_scratch, st));
         }
         rc = flowtree_stage(ds, S, nq, ds->s_cand.as<int64_t>(), m, m, ds->s_vals2.as<double>(), m, st);
         if (rc) return rc;
         StageTimer tm(ds, FTI_ST_SELK, st);
         FTI_CUDA(fti_launch_select(ds->s_vals2.as<double>(), m, ds->s_cand.as<int64_t>(), m, m, nq, k, d_ids, d_val,
-                                   k, st));
+                                   k, sel_scratch, st));
     }
     if (!dev_out) {
         FTI_CUDA(cudaMemcpyAsync(out_ids, d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, st));

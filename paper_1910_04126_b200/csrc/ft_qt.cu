@@ -245,12 +245,8 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 if (h >= 0) id = idxs[h];
             }
             unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
-            while (hm) {
-                const int l = __ffs(hm) - 1;
-                hm &= hm - 1;
-                const int idl = __shfl_sync(0xffffffffu, id, l);
-                const uint32_t mmu = __shfl_sync(0xffffffffu, rec.y, l);
-                const uint2 e = ent[idl];
+            // two hits per iteration: independent lookup chains the scheduler can overlap
+            auto visit = [&](const uint2 e, uint32_t mmu) {
                 if ((e.x >> lane) & 1u) {
                     const uint32_t p = post[e.y + __popc(e.x & lt)];
                     // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
@@ -258,6 +254,21 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                     const uint32_t wm = W32 * (p & 0xFFFFu);
                     acc += (unsigned long long)(um < wm ? um : wm) << (a.d_star - (int)((p >> 16) & 63u));
                 }
+            };
+            while (hm) {
+                const int l1 = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const int l2 = hm ? __ffs(hm) - 1 : l1;
+                const bool two = hm != 0u;
+                hm &= hm - 1;
+                const int id1 = __shfl_sync(0xffffffffu, id, l1);
+                const uint32_t m1 = __shfl_sync(0xffffffffu, rec.y, l1);
+                const int id2 = __shfl_sync(0xffffffffu, id, l2);
+                const uint32_t m2 = __shfl_sync(0xffffffffu, rec.y, l2);
+                const uint2 e1 = ent[id1];
+                const uint2 e2 = two ? ent[id2] : make_uint2(0u, 0u);
+                visit(e1, m1);
+                visit(e2, m2);
             }
         }
         if (lane < nqc) {

@@ -8,6 +8,7 @@
 // memory.  Exact for any amount of ties — the Quadtree keys at d = 300 take only a few hundred
 // distinct values over 10^5 docs.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ft_device.cuh"
 
@@ -26,10 +27,111 @@ __device__ __forceinline__ unsigned digit_of(unsigned long long hi, uint32_t lo,
     return t < 8 ? (unsigned)((hi >> (56 - 8 * t)) & 255ull) : (unsigned)((lo >> (24 - 8 * (t - 8))) & 255u);
 }
 
+
+// Sample-threshold selection (the common case): sort a strided sample of the keys, take a key a
+// safe margin above the sample's k/L quantile as threshold t, gather every key ≤ t (exact count,
+// warp-aggregated positions) and bitonic-sort the gathered (key, id) pairs; the first k are the
+// answer.  Exact whenever k ≤ count(≤ t) ≤ capacity; otherwise the row is flagged for the radix
+// kernel.  Two passes over the row instead of up to twelve.
+constexpr int SEL_CAP = 8192;
+constexpr int SEL_SAMPLE = 4096;
+
+__device__ void sort_pairs(unsigned long long* h, uint32_t* l, int P) {
+    for (int kb = 2; kb <= P; kb <<= 1) {
+        for (int j = kb >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long ah = h[i], bh2 = h[ixj];
+                    const uint32_t al = l[i], bl2 = l[ixj];
+                    const bool gt = (ah > bh2) || (ah == bh2 && al > bl2);
+                    const bool up = (i & kb) == 0;
+                    if (gt == up) { h[i] = bh2; h[ixj] = ah; l[i] = bl2; l[ixj] = al; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ vals, int64_t vals_ld,
+                                                     const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L,
+                                                     int k, int64_t* __restrict__ out_ids,
+                                                     double* __restrict__ out_val, int64_t out_ld,
+                                                     int* __restrict__ redo, int* __restrict__ nredo) {
+    extern __shared__ unsigned long long sbuf[];
+    unsigned long long* bh = sbuf;                      // SEL_CAP
+    uint32_t* bl = (uint32_t*)(sbuf + SEL_CAP);         // SEL_CAP
+    __shared__ unsigned long long s_thr;
+    __shared__ int s_cnt;
+    const int row = blockIdx.x;
+    const double* v = vals + (int64_t)row * vals_ld;
+    const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
+    const int kk = (int)min((int64_t)k, L);
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_cnt = 0;
+    unsigned long long thr = ~0ull;
+    if (L > SEL_CAP) {
+        // strided sample of S keys, sorted; threshold = sample key at the k/L quantile + margin
+        const int S = SEL_SAMPLE;
+        for (int j = threadIdx.x; j < S; j += blockDim.x) bh[j] = okey(v[(int64_t)j * L / S]);
+        __syncthreads();
+        fti_bitonic_sort_u64(bh, S);
+        if (threadIdx.x == 0) {
+            const double ex = (double)kk * S / (double)L;
+            const int ti = min(S - 1, (int)(ex + 4.0 * sqrt(ex) + 8.0));
+            s_thr = bh[ti];
+        }
+        __syncthreads();
+        thr = s_thr;
+    }
+    // gather every key ≤ thr (all of them when L ≤ SEL_CAP)
+    for (int64_t i0 = 0; i0 < L; i0 += blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        unsigned long long hi = 0;
+        bool sel = false;
+        if (i < L) {
+            hi = okey(v[i]);
+            sel = hi <= thr;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_cnt, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sel) {
+            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (pos < SEL_CAP) { bh[pos] = hi; bl[pos] = id ? (uint32_t)id[i] : (uint32_t)i; }
+        }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (cnt < kk || cnt > SEL_CAP) {       // threshold too low or too many ties: radix kernel
+        if (threadIdx.x == 0) redo[atomicAdd(nredo, 1)] = row;
+        return;
+    }
+    const int P = fti_pow2_at_least(max(cnt, 2));
+    for (int i = cnt + threadIdx.x; i < P; i += blockDim.x) { bh[i] = ~0ull; bl[i] = 0xFFFFFFFFu; }
+    __syncthreads();
+    sort_pairs(bh, bl, P);
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        int64_t oid = -1;
+        double ov = __longlong_as_double(0x7ff0000000000000ll);
+        if (t < kk) {
+            ov = okey_inv(bh[t]);
+            oid = (int64_t)bl[t];
+        }
+        out_ids[(int64_t)row * out_ld + t] = oid;
+        out_val[(int64_t)row * out_ld + t] = ov;
+    }
+}
+
+// MSD radix selection (rows the sample-threshold pass could not finish; `rows_list` null: all rows)
 __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals, int64_t vals_ld,
                                                 const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L, int k,
                                                 int64_t* __restrict__ out_ids, double* __restrict__ out_val,
-                                                int64_t out_ld, int P) {
+                                                int64_t out_ld, int P, const int* __restrict__ rows_list,
+                                                const int* __restrict__ nrows_list) {
+    if (rows_list && (int)blockIdx.x >= *nrows_list) return;
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;               // P
     uint32_t* bl = (uint32_t*)(sbuf + P);        // P
@@ -37,7 +139,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
     __shared__ unsigned long long s_ph, s_mh;
     __shared__ uint32_t s_pl, s_ml;
     __shared__ int s_need, s_done, s_cnt;
-    const int row = blockIdx.x;
+    const int row = rows_list ? rows_list[blockIdx.x] : blockIdx.x;
     const double* v = vals + (int64_t)row * vals_ld;
     const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
     const int kk = (int)std::min<int64_t>(k, L);
@@ -129,14 +231,32 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
 
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
-                              cudaStream_t st) {
+                              int* d_scratch, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
     int kk = (int)std::min<int64_t>(k, L);
     int P = fti_pow2_at_least(std::max(kk, 2));
     size_t smem = (size_t)P * 12 + 16;
     cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P);
-    fti_count_launches(1);
+    if (getenv("FT_SELECT_RADIX")) {   // test hook: the radix kernel for every row
+        k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P,
+                                          nullptr, nullptr);
+        fti_count_launches(1);
+        return cudaGetLastError();
+    }
+    // pass 1: sample threshold + gather + sort; rows it cannot finish are listed in d_scratch[1..]
+    int* nredo = d_scratch;
+    int* redo = d_scratch + 1;
+    e = cudaMemsetAsync(nredo, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    const size_t smem_f = (size_t)SEL_CAP * 12;
+    e = cudaFuncSetAttribute(k_select_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+    if (e != cudaSuccess) return e;
+    k_select_fast<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo,
+                                             nredo);
+    // pass 2: MSD radix selection of the listed rows (CTAs past the list exit at once)
+    k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P, redo,
+                                      nredo);
+    fti_count_launches(2);
     return cudaGetLastError();
 }

@@ -270,9 +270,14 @@ def test_knn_tiny(ft, prefilter_m):
         assert_ft_close(vals[q], [ftv[i] for i in ids[q]])
 
 
-def test_knn_prefilter_ids_exact(ft):
-    """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id)."""
-    wl = get_workload("reviews", n_docs=5000, n_queries=4)
+@pytest.mark.parametrize("n_docs,radix", [(5000, False), (20000, False), (20000, True)])
+def test_knn_prefilter_ids_exact(ft, monkeypatch, n_docs, radix):
+    """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id), in
+    order.  n ≤ 8192 sorts the whole row; n = 20000 takes the sample-threshold path (the Quadtree
+    values at d = 300 are heavily tied); FT_SELECT_RADIX=1 forces the MSD radix kernel."""
+    if radix:
+        monkeypatch.setenv("FT_SELECT_RADIX", "1")
+    wl = get_workload("reviews", n_docs=n_docs, n_queries=4)
     T = oracle_tree(wl)
     ix, ds = _setup(ft, wl)
     m = 300
