@@ -150,7 +150,7 @@ struct ft_dataset {
     unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd;
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_layout(LayoutArgs a) {
             A_part += (unsigned long long)mass << sh;
             is_mn = a.node_count[node] >= 2;
             if (is_mn) atomicAdd(&mn_hist[dep], 1);
-            if (a.fill) a.qt[a.qt_off[doc] + g] = make_uint2(node, mass);
+            if (a.fill) a.qt[a.qt_off[doc] + g] = make_uint2(node, mass | ((uint32_t)dep << 16));   // mass | depth << 16
         }
         int tot;
         int r = mn_run + fti_block_exclusive_sum(is_mn, tmp, &tot);
@@ -378,7 +378,7 @@ extern "C" void ft_dataset_free(ft_dataset* ds) {
     if (ds->prof_units) cudaFree(ds->prof_units);
     DevBuf* bufs[] = {&ds->s_qoff, &ds->s_qids, &ds->s_qw, &ds->s_qblock, &ds->s_docs, &ds->s_vals, &ds->s_vals2,
                       &ds->s_cand, &ds->s_outid, &ds->s_outval, &ds->s_map, &ds->s_rows, &ds->s_rowcnt,
-                      &ds->s_table, &ds->s_flow, &ds->s_flowcnt, &ds->s_vlist, &ds->s_chunk, &ds->s_rowbase, &ds->s_bsplit, &ds->s_ny, &ds->s_tiles, &ds->s_qinfo, &ds->s_wdesc, &ds->s_wrow, &ds->s_sel};
+                      &ds->s_table, &ds->s_flow, &ds->s_flowcnt, &ds->s_vlist, &ds->s_chunk, &ds->s_rowbase, &ds->s_bsplit, &ds->s_ny, &ds->s_tiles, &ds->s_qinfo, &ds->s_wdesc, &ds->s_wrow, &ds->s_sel, &ds->s_chunkd};
     for (DevBuf* b : bufs) b->release();
     delete ds;
 }

@@ -20,6 +20,7 @@
 // posting and accumulates ω·min(U m_μ, W m_ν) in a u64 register — no atomics, no per-query
 // probing.  Lane q then finalises the value of (q, doc).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ft_device.cuh"
 
@@ -188,6 +189,78 @@ __global__ void __launch_bounds__(1024) k_qt_chunk(const uint8_t* __restrict__ q
     }
 }
 
+// Dense chunk structure, one CTA per chunk: the union of the chunk's query nodes as a bitmap over
+// all node ids with per-word ranks, and a dense [union][32 lanes] u16 mass array.  Chunks whose
+// union exceeds the capacity keep flag 0 and are scanned with the hash structure.
+struct DenseGeom {
+    int mw;          // bitmap words = ceil(M / 32)
+    int cap;         // max union size (0: dense path disabled)
+    size_t stride;   // bytes per chunk: header | bits[mw] | rank[mw] | post[cap][32]
+};
+
+struct DenseHdr {
+    uint32_t flag, nU, pad0, pad1;
+};
+
+__global__ void __launch_bounds__(1024) k_qt_dense(const uint8_t* __restrict__ qblock, QueryLayout L, int32_t nq,
+                                                   DenseGeom dg, uint8_t* __restrict__ dchunks) {
+    extern __shared__ uint32_t sd[];
+    uint32_t* bits = sd;              // mw
+    uint32_t* rank = sd + dg.mw;      // mw
+    __shared__ int tmp[32];
+    const int c = blockIdx.x;
+    const int q0 = c * QT_QC;
+    const int nqc = min(QT_QC, nq - q0);
+    uint8_t* out = dchunks + (size_t)c * dg.stride;
+    DenseHdr* hdr = (DenseHdr*)out;
+    for (int i = threadIdx.x; i < dg.mw; i += blockDim.x) bits[i] = 0u;
+    __syncthreads();
+    const int slots = L.nh_cap;
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        atomicOr(&bits[e.x >> 5], 1u << (e.x & 31u));
+    }
+    __syncthreads();
+    int run = 0;
+    for (int b0 = 0; b0 < dg.mw; b0 += blockDim.x) {
+        const int w = b0 + threadIdx.x;
+        const int v = w < dg.mw ? __popc(bits[w]) : 0;
+        int tot;
+        const int r = run + fti_block_exclusive_sum(v, tmp, &tot);
+        if (w < dg.mw) rank[w] = (uint32_t)r;
+        run += tot;
+    }
+    __syncthreads();
+    const int nU = run;
+    if (nU > dg.cap) {
+        if (threadIdx.x == 0) { hdr->flag = 0u; hdr->nU = (uint32_t)nU; }
+        return;
+    }
+    uint32_t* gbits = (uint32_t*)(out + sizeof(DenseHdr));
+    uint32_t* grank = gbits + dg.mw;
+    uint16_t* gpost = (uint16_t*)(grank + dg.mw);
+    for (int i = threadIdx.x; i < dg.mw; i += blockDim.x) { gbits[i] = bits[i]; grank[i] = rank[i]; }
+    for (int i = threadIdx.x; i < nU * QT_QC / 2; i += blockDim.x) ((uint32_t*)gpost)[i] = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        const uint32_t bw = bits[e.x >> 5], bpos = e.x & 31u;
+        const uint32_t id = rank[e.x >> 5] + __popc(bw & ((1u << bpos) - 1u));
+        gpost[id * QT_QC + ql] = (uint16_t)(e.y & 0xFFFFu);
+    }
+    if (threadIdx.x == 0) { hdr->flag = 1u; hdr->nU = (uint32_t)nU; }
+}
+
 struct QtArgs {
     const uint32_t* qt_off;
     const uint2* qt;
@@ -195,6 +268,8 @@ struct QtArgs {
     const unsigned long long* A;
     const uint8_t* chunks;
     ChunkGeom g;
+    const uint8_t* dchunks;
+    DenseGeom dg;
     int32_t nq;
     const int64_t* docs;
     int64_t n_docs;
@@ -206,7 +281,95 @@ struct QtArgs {
     uint32_t* err;
 };
 
-// the doc scan of one CTA; SMEM: the masks/offsets and postings are in shared memory (the common
+// lane q: QT(q, doc) = (U A + W B_q − 2 acc) · 2^{ℓ_root − D*} / (W U), exact u64 numerator, two
+// correctly rounded FP64 operations (NaN for an invalid query or an overflowing numerator)
+__device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int64_t dp,
+                                         unsigned long long acc, uint32_t W32, unsigned long long A) {
+    const int lane = threadIdx.x & 31;
+    if (lane >= nqc) return;
+    const int q = blockIdx.y * QT_QC + lane;
+    const unsigned long long Uq = sh.U[lane], Bq = sh.B[lane], W = W32;
+    double val;
+    bool bad = !sh.ok[lane];
+    bad |= __umul64hi(Uq, A) != 0ull || __umul64hi(W, Bq) != 0ull;
+    const unsigned long long ua = Uq * A, wb = W * Bq;
+    const unsigned long long tot = ua + wb;
+    bad |= tot < ua;
+    const unsigned long long num = tot - (acc << 1);
+    if (!bad && num >= (1ull << 53)) {
+        bad = true;
+        atomicOr(a.err, FTI_ERR_OVERFLOW);
+    }
+    if (bad) {
+        val = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+        const double scaled = scalbn((double)num, a.l_root - a.d_star);
+        val = __ddiv_rn(scaled, (double)(Uq * W));
+    }
+    a.out[(int64_t)q * a.out_ld + dp] = val;
+}
+
+// Dense chunk structure (when the chunk's node union is small and the tree's node ids fit a
+// shared-memory bitmap): membership of a doc node is one bit test, its union index a rank
+// (per-word prefix + popc), and the chunk's masses are a dense [union][32 lanes] u16 array — a
+// query without the node reads 0 — so every hit costs one conflict-free LDS per lane, no mask
+// test, no posting search.  The node's depth rides in the doc record (mass | depth << 16).
+__device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* __restrict__ bits,
+                                              const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
+                                              const ChunkHdr& sh, int nqc) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t U32 = sh.U[lane];
+    const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
+    const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
+    for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
+        const int64_t doc = a.docs ? a.docs[dp] : dp;
+        if (doc < 0 || doc >= a.n) {
+            if (lane < nqc)
+                a.out[(int64_t)(blockIdx.y * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+            if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
+            continue;
+        }
+        const uint32_t r0 = a.qt_off[doc], r1 = a.qt_off[doc + 1];
+        const uint32_t W32 = a.W[doc];
+        const unsigned long long A = a.A[doc];
+        unsigned long long acc = 0;
+        auto term = [&](uint32_t mnu, uint32_t y) {
+            // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
+            const uint32_t um = U32 * (y & 0xFFFFu);
+            const uint32_t wm = W32 * mnu;
+            acc += (unsigned long long)(um < wm ? um : wm) << (a.d_star - (int)(y >> 16));
+        };
+        for (uint32_t rb = r0; rb < r1; rb += 32) {
+            const uint32_t r = rb + lane;
+            uint2 rec = make_uint2(0u, 0u);
+            int id = -1;
+            if (r < r1) {
+                rec = a.qt[r];
+                const uint32_t bw = bits[rec.x >> 5], bpos = rec.x & 31u;
+                if ((bw >> bpos) & 1u) id = (int)(rank[rec.x >> 5] + __popc(bw & ((1u << bpos) - 1u)));
+            }
+            unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
+            while (hm) {
+                const int l1 = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const int l2 = hm ? __ffs(hm) - 1 : l1;
+                const bool two = hm != 0u;
+                hm &= hm - 1;
+                const int id1 = __shfl_sync(0xffffffffu, id, l1);
+                const uint32_t y1 = __shfl_sync(0xffffffffu, rec.y, l1);
+                const int id2 = __shfl_sync(0xffffffffu, id, l2);
+                const uint32_t y2 = __shfl_sync(0xffffffffu, rec.y, l2);
+                const uint32_t p1 = post[id1 * QT_QC + lane];
+                const uint32_t p2 = two ? (uint32_t)post[id2 * QT_QC + lane] : 0u;
+                term(p1, y1);
+                term(p2, y2);
+            }
+        }
+        qt_store(a, sh, nqc, dp, acc, W32, A);
+    }
+}
+
+// the doc scan of one CTA (hash structure); SMEM: the masks/offsets and postings are in shared memory (the common
 // case), so every lookup is an LDS rather than a generic load
 template <bool SMEM>
 __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restrict__ keys,
@@ -217,9 +380,6 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
-    const unsigned long long Uq = sh.U[lane];
-    const unsigned long long Bq = sh.B[lane];
-    const bool okq = lane < nqc && sh.ok[lane];
     const int q = blockIdx.y * QT_QC + lane;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
@@ -232,7 +392,6 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
         }
         const uint32_t r0 = a.qt_off[doc], r1 = a.qt_off[doc + 1];
         const uint32_t W32 = a.W[doc];
-        const unsigned long long W = W32;
         const unsigned long long A = a.A[doc];
         unsigned long long acc = 0;
         for (uint32_t rb = r0; rb < r1; rb += 32) {
@@ -250,7 +409,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 if ((e.x >> lane) & 1u) {
                     const uint32_t p = post[e.y + __popc(e.x & lt)];
                     // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
-                    const uint32_t um = U32 * mmu;
+                    const uint32_t um = U32 * (mmu & 0xFFFFu);
                     const uint32_t wm = W32 * (p & 0xFFFFu);
                     acc += (unsigned long long)(um < wm ? um : wm) << (a.d_star - (int)((p >> 16) & 63u));
                 }
@@ -271,26 +430,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 visit(e2, m2);
             }
         }
-        if (lane < nqc) {
-            double val;
-            bool bad = !okq;
-            bad |= __umul64hi(Uq, A) != 0ull || __umul64hi(W, Bq) != 0ull;
-            const unsigned long long ua = Uq * A, wb = W * Bq;
-            const unsigned long long tot = ua + wb;
-            bad |= tot < ua;
-            const unsigned long long num = tot - (acc << 1);
-            if (!bad && num >= (1ull << 53)) {
-                bad = true;
-                atomicOr(a.err, FTI_ERR_OVERFLOW);
-            }
-            if (bad) {
-                val = __longlong_as_double(0x7ff8000000000000ll);
-            } else {
-                const double scaled = scalbn((double)num, a.l_root - a.d_star);
-                val = __ddiv_rn(scaled, (double)(Uq * W));
-            }
-            a.out[(int64_t)q * a.out_ld + dp] = val;
-        }
+        qt_store(a, sh, nqc, dp, acc, W32, A);
     }
 }
 
@@ -303,8 +443,24 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
     uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
     uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
     const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
-    if (threadIdx.x == 0) sh = *(const ChunkHdr*)src;
+    __shared__ DenseHdr dh;
+    const uint8_t* dsrc = a.dchunks ? a.dchunks + (size_t)blockIdx.y * a.dg.stride : nullptr;
+    if (threadIdx.x == 0) {
+        sh = *(const ChunkHdr*)src;
+        dh = dsrc ? *(const DenseHdr*)dsrc : DenseHdr{0u, 0u, 0u, 0u};
+    }
     __syncthreads();
+    if (dh.flag) {
+        uint32_t* bits = sm;
+        uint32_t* rank = sm + a.dg.mw;
+        uint16_t* post = (uint16_t*)(rank + a.dg.mw);
+        const uint32_t* gb = (const uint32_t*)(dsrc + sizeof(DenseHdr));
+        const int nwords = 2 * a.dg.mw + (int)dh.nU * QT_QC / 2;    // bits | rank | post, contiguous
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) sm[i] = gb[i];
+        __syncthreads();
+        qt_scan_dense(a, bits, rank, post, sh, (int)sh.nq);
+        return;
+    }
     const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
     const uint2* ge = (const uint2*)(src + g.off_mask);
     const uint32_t* gp = (const uint32_t*)(src + g.off_post);
@@ -344,14 +500,33 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     e = cudaFuncSetAttribute(k_qt_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
     if (e != cudaSuccess) return e;
     k_qt_chunk<<<nchunks, 1024, smem_c, st>>>(d_qblock, L, nq, g, ds->s_chunk.as<uint8_t>(), ds->err_dev);
+    // dense structure: node-id bitmap + ranks in shared memory (M ≤ ~393k nodes), union ≤ cap
+    DenseGeom dg{};
+    dg.mw = (int)((ds->ix->M + 31) / 32);
+    const size_t dense_budget = 200 * 1024;
+    dg.cap = 0;
+    if ((size_t)dg.mw * 8 <= 96 * 1024 && !getenv("FT_QT_HASH"))   // FT_QT_HASH=1: test hook, hash path only
+        dg.cap = (int)std::min<size_t>(2048, (dense_budget - (size_t)dg.mw * 8) / (QT_QC * 2)) & ~31;
+    dg.stride = (sizeof(DenseHdr) + (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 15) / 16 * 16;
+    if (dg.cap > 0) {
+        e = ds->s_chunkd.reserve(dg.stride * (size_t)nchunks);
+        if (e != cudaSuccess) return e;
+        const size_t smem_d = (size_t)dg.mw * 8;
+        e = cudaFuncSetAttribute(k_qt_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        if (e != cudaSuccess) return e;
+        k_qt_dense<<<nchunks, 1024, smem_d, st>>>(d_qblock, L, nq, dg, ds->s_chunkd.as<uint8_t>());
+        fti_count_launches(1);
+    }
     QtArgs a{};
     a.qt_off = ds->qt_off; a.qt = ds->qt; a.W = ds->W; a.A = ds->A;
     a.chunks = ds->s_chunk.as<uint8_t>(); a.g = g;
+    a.dchunks = dg.cap > 0 ? ds->s_chunkd.as<uint8_t>() : nullptr; a.dg = dg;
     a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
     a.err = ds->err_dev;
-    const size_t smem = 4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap;
+    const size_t smem = std::max<size_t>(4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap,
+                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 : 0);
     e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int ctas_per_sm = 0;

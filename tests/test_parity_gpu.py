@@ -221,6 +221,19 @@ def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
         assert np.array_equal(f_a[key], f_b[key])
 
 
+@pytest.mark.parametrize("name", ["image", "text", "reviews"])
+def test_qt_dense_matches_hash(ft, monkeypatch, name):
+    """The Quadtree kernel scans a chunk with the dense bitmap structure when its node union is
+    small and with the hash structure otherwise (FT_QT_HASH=1 forces the hash); both are exact,
+    so the values must be bit-identical (the oracle comparison is in the parity tests)."""
+    wl = get_workload(name, n_docs=3000, n_queries=40)
+    ix, ds = _setup(ft, wl)
+    a = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    monkeypatch.setenv("FT_QT_HASH", "1")
+    b = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    assert np.array_equal(a, b)
+
+
 def test_distance_table_accuracy(ft):
     """FT(δ_x, δ_y) = ||x − y|| (one triple), so single-point docs/queries expose the tensor-core
     distance table directly; compare with FP64 distances.  Error model: the Gram
