@@ -78,16 +78,19 @@ for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one
         summ.append(f"### {short}")
         for m, (v, u) in ms.items():
             summ.append(f"  {m} = {v} {u}")
-        if short == "k_qt" and rep == "prof_qt.ncu-rep":
+        key = {("k_qt", "prof_qt.ncu-rep"): "quadtree", ("k_dist_tc", "prof_knn.ncu-rep"): "dist_table",
+               ("k_flowtree", "prof_knn.ncu-rep"): "flowtree"}.get((short.split("<")[0], rep))
+        if key and f"{key}_dram_bytes_per_launch" not in traffic:
             rd = float(ms["dram__bytes_read.sum"][0].replace(",", ""))
             wr = float(ms["dram__bytes_write.sum"][0].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            traffic["k_qt_dram_bytes_per_launch"] = rd * scale.get(ms["dram__bytes_read.sum"][1], 1) + \
+            traffic[f"{key}_dram_bytes_per_launch"] = rd * scale.get(ms["dram__bytes_read.sum"][1], 1) + \
                 wr * scale.get(ms["dram__bytes_write.sum"][1], 1)
-            traffic["k_qt_launch_pairs"] = 1000 * 100000
         summ.append("")
 open(os.path.join(PROF, f"{rnd}_ncu_summary.txt"), "w").write("\n".join(summ) + "\n")
 if traffic:
-    traffic["source"] = f"profiles/{rnd}_ncu_summary.txt (ncu --set full of the bench-batch k_qt launch)"
+    traffic["source"] = (f"profiles/{rnd}_ncu_summary.txt: dram read+write of one ncu --set full launch (k_qt: the "
+                         "1000-query bench batch; k_dist_tc / k_flowtree: the first query chunk of kprof knn, the "
+                         "same chunk size the bench uses)")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     print(traffic)
