@@ -56,6 +56,9 @@ struct FtArgs {
     int use_bitmap;   // query vocab lookup by bitmap + rank (N small enough), else by hash
     int nwords;       // bitmap words = ceil(N / 32)
     unsigned long long* units;   // profiler: Σ pairs (8 s_doc + 16) algorithmic bytes, or null
+    const uint32_t* fb_list;     // list mode: [nq][fb_cap] doc positions handed over by k_ftx
+    const uint32_t* fb_cnt;      // [nq]
+    int64_t fb_cap;
 };
 
 constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
@@ -308,9 +311,15 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
     c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
 
     unsigned long long ubytes = 0;
+    // range mode: this CTA's contiguous doc range; list mode: the pairs k_ftx handed over
+    const bool list_mode = a.fb_list != nullptr;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
-    for (int64_t dp = d0 + warp; dp < d1; dp += FT_WARPS) {
+    const int64_t e0 = list_mode ? (int64_t)blockIdx.x * FT_WARPS + warp : d0 + warp;
+    const int64_t e1 = list_mode ? (int64_t)a.fb_cnt[q] : d1;
+    const int64_t estep = list_mode ? (int64_t)gridDim.x * FT_WARPS : FT_WARPS;
+    for (int64_t e = e0; e < e1; e += estep) {
+        const int64_t dp = list_mode ? (int64_t)a.fb_list[(int64_t)q * a.fb_cap + e] : e;
         const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
         double* outp = a.out ? a.out + (int64_t)q * a.out_ld + dp : nullptr;
         if (!qok || doc < 0 || doc >= a.n) {
@@ -431,6 +440,22 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     const size_t ysm = a.small_d ? (size_t)a.Sq * a.d * 4 : 0;
     size_t smem = (size_t)a.Sq * 8 + lookup + ysm + (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
     cudaError_t e;
+    // exhaustive scoring with a distance table and a star-like tree: the lane-per-query chunk kernel
+    // (ft_flowx.cu) scores every pair it can and lists the rest for this kernel (list mode)
+    if (!d_flow && !d_docs && tab.table && !tab.map && a.use_bitmap && ds->n_mn <= 2 * ds->n &&
+        L.smax <= FTX_MAX_SQ && !getenv("FT_GENERAL_ONLY")) {
+        uint32_t* fl = nullptr;
+        uint32_t* fc = nullptr;
+        e = fti_launch_ftx(ds, L, d_qblock, nq, n_docs, tab, d_out, out_ld, &fl, &fc, st);
+        if (e == cudaSuccess) {
+            a.fb_list = fl;
+            a.fb_cnt = fc;
+            a.fb_cap = n_docs;
+            bx = std::max<int64_t>(1, std::min<int64_t>(32, (148 * 4 + nq - 1) / nq));
+        } else if (e != cudaErrorNotSupported) {
+            return e;
+        }
+    }
     if (d_flow) {
         e = cudaFuncSetAttribute(k_flowtree<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -150,7 +150,7 @@ struct ft_dataset {
     unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
     DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_ftxchunk;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -172,6 +172,12 @@ struct FtTable {
     int64_t rows_cap = 0;
     int32_t ld = 0;
 };
+// exhaustive Flowtree, lane = query of a 32-query chunk (ft_flowx.cu); pairs it cannot score are
+// listed per query in *fb_list / *fb_cnt (capacity n_docs per query) for the warp kernel
+#define FTX_MAX_SQ 256
+cudaError_t fti_launch_ftx(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t n_docs,
+                           const FtTable& tab, double* d_out, int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt,
+                           cudaStream_t st);
 cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab,
                           double* d_out, int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap,

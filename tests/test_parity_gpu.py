@@ -221,6 +221,22 @@ def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
         assert np.array_equal(f_a[key], f_b[key])
 
 
+@pytest.mark.parametrize("name,nq", [("text", 40), ("reviews", 70)])
+def test_chunked_flowtree_matches_warp_kernel(ft, monkeypatch, name, nq):
+    """Exhaustive scoring runs the lane-per-query chunk kernel (pairs sharing an M-node are listed
+    for the warp kernel); FT_GENERAL_ONLY=1 runs the warp kernel for every pair.  The flows are the
+    same triples, so the values agree to FP summation order; ragged chunks (nq not a multiple of
+    32) included."""
+    wl = get_workload(name, n_docs=2500, n_queries=nq)
+    ix, ds = _setup(ft, wl)
+    a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    assert np.all(np.isfinite(a))
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
+    assert np.array_equal(a == 0.0, b == 0.0)
+
+
 @pytest.mark.parametrize("name", ["image", "text", "reviews"])
 def test_qt_dense_matches_hash(ft, monkeypatch, name):
     """The Quadtree kernel scans a chunk with the dense bitmap structure when its node union is
