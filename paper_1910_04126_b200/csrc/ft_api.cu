@@ -197,36 +197,40 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
     // query chunks bounded by the worst-case table allocation (tables are written compactly)
     const size_t nwords = (size_t)(ix->N + 31) / 32;
-    const size_t per_q = (size_t)rows_cap * ld * 4 + (use_map ? nwords * 8 + (size_t)rows_cap * 4 + 12 : 0);
+    const size_t per_q = (size_t)rows_cap * ld * 4;
     const size_t budget = (size_t)3 << 30;
     const int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
     if (use_map) {
-        FTI_RES(ds->s_map, (size_t)qch * nwords * 8);
-        FTI_RES(ds->s_rows, (size_t)qch * rows_cap * 4);
-        FTI_RES(ds->s_rowcnt, (size_t)qch * 4);
+        // candidate vocabulary of every query in one launch (a CTA per query fills the GPU); the
+        // per-chunk table placement is a prefix over the chunk's row counts
+        FTI_RES(ds->s_map, (size_t)nq * nwords * 8);
+        FTI_RES(ds->s_rows, (size_t)nq * rows_cap * 4);
+        FTI_RES(ds->s_rowcnt, (size_t)nq * 4);
         FTI_RES(ds->s_rowbase, (size_t)qch * 8);
+        StageTimer tm(ds, FTI_ST_VMAP, st);
+        FTI_CUDA(fti_launch_vocab_map(ds, nq, d_docs, docs_ld, n_docs, ds->s_map.as<uint2>(), ds->s_rows.as<int32_t>(),
+                                      ds->s_rowcnt.as<int32_t>(), rows_cap, st));
     }
     for (int32_t q0 = 0; q0 < nq; q0 += qch) {
         const int32_t nqc = std::min(qch, nq - q0);
         const uint8_t* qb = S.qblock + (size_t)q0 * S.L.stride;
         const int64_t* dq = d_docs ? d_docs + (int64_t)q0 * docs_ld : nullptr;
+        const int32_t* rows_c = use_map ? ds->s_rows.as<int32_t>() + (int64_t)q0 * rows_cap : nullptr;
+        const int32_t* rowcnt_c = use_map ? ds->s_rowcnt.as<int32_t>() + q0 : nullptr;
         FtTable tab;
         tab.table = ds->s_table.as<float>();
         tab.rows_cap = rows_cap;
         tab.ld = ld;
         if (use_map) {
             StageTimer tm(ds, FTI_ST_VMAP, st);
-            FTI_CUDA(fti_launch_vocab_map(ds, nqc, dq, docs_ld, n_docs, ds->s_map.as<uint2>(),
-                                          ds->s_rows.as<int32_t>(), ds->s_rowcnt.as<int32_t>(), rows_cap,
-                                          ds->s_rowbase.as<int64_t>(), st));
-            tab.map = ds->s_map.as<uint2>();
+            FTI_CUDA(fti_launch_row_base(rowcnt_c, nqc, ds->s_rowbase.as<int64_t>(), st));
+            tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
             tab.row_base = ds->s_rowbase.as<int64_t>();
         }
         {
             StageTimer tm(ds, FTI_ST_DIST, st);
-            FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, use_map ? ds->s_rows.as<int32_t>() : nullptr,
-                                           use_map ? ds->s_rowcnt.as<int32_t>() : nullptr, rows_cap,
+            FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, rows_c, rowcnt_c, rows_cap,
                                            use_map ? ds->s_rowbase.as<int64_t>() : nullptr,
                                            ds->s_table.as<float>(), ld, st));
         }

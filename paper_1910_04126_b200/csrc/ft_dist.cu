@@ -761,7 +761,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
 
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
-                                 int64_t* d_row_base, cudaStream_t st) {
+                                 cudaStream_t st) {
     if (nq <= 0) return cudaSuccess;
     const int64_t nwords = (ds->ix->N + 31) / 32;
     const size_t smem = (size_t)nwords * 4;
@@ -770,7 +770,13 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
     if (e != cudaSuccess) return e;
     k_vocab<<<nq, 1024, smem, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, nwords, d_map, d_rows, d_rowcnt,
                                     rows_cap);
+    fti_count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, int32_t nq, int64_t* d_row_base, cudaStream_t st) {
+    if (nq <= 0) return cudaSuccess;
     k_row_base<<<1, 32, 0, st>>>(d_rowcnt, nq, d_row_base);
-    fti_count_launches(2);
+    fti_count_launches(1);
     return cudaGetLastError();
 }
