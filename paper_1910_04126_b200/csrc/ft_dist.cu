@@ -548,15 +548,15 @@ __global__ void __launch_bounds__(256) k_dist_prep(DistArgs a) {
     for (int j = threadIdx.x; j < NCB; j += blockDim.x) {
         const uint32_t y = j < nb ? (qitems[a.cb * NCB + j].x & FTI_VOCAB_MASK) : 0xFFFFFFFFu;
         yid[j] = y;
-        a.ny[(int64_t)q * NCB + j] = j < nb ? a.xnorm[y] : 0.f;
+        if (blockIdx.y == 0) a.ny[(int64_t)q * NCB + j] = j < nb ? a.xnorm[y] : 0.f;
     }
     __syncthreads();
     if (!np) return;
     const uint32_t b_bytes = (uint32_t)np * KC * 4;
     uint8_t* bq = (uint8_t*)a.bsplit + 16 * (size_t)qi.x;
-    // thread per (chunk, row, 4-group)
+    // CTA (query, K-chunk slice); thread per (chunk, row, 4-group)
     const int groups = a.nch * np * (KC / 4);
-    for (int e = threadIdx.x; e < groups; e += blockDim.x) {
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < groups; e += gridDim.y * blockDim.x) {
         const int g = e % (KC / 4);
         const int j = (e / (KC / 4)) % np;
         const int cc = e / ((KC / 4) * np);
@@ -742,7 +742,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
         a.cb = cb;
         k_tile_plan<<<1, 1024, 0, st>>>(a, ix->d, ds->units_ptr(FTI_ST_DIST));
         k_tiles<<<dim3((unsigned)nq, slices), TM, 0, st>>>(a);
-        k_dist_prep<<<nq, 256, 0, st>>>(a);
+        k_dist_prep<<<dim3((unsigned)nq, (unsigned)std::min(a.nch, 8)), 256, 0, st>>>(a);
         kern<<<148, NTHREADS, smem, st>>>(a);
         fti_count_launches(4);
         if (dbg) {
