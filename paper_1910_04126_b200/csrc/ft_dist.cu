@@ -49,7 +49,8 @@ constexpr int NCOPY = 128;              // copy threads (warps 0-3)
 constexpr int NCONV = 128;              // converter threads: one tile row each (warps 4-7)
 constexpr int NLOAD = NCOPY + NCONV;
 constexpr int MMA_WARP = NLOAD / 32;    // warp 8
-constexpr int NTHREADS = NLOAD + 32 + 128;   // + 1 MMA + 4 epilogue warps
+constexpr int NEPI = 8;                 // epilogue warps: 2 per TMEM lane quarter, alternating 16-column blocks
+constexpr int NTHREADS = NLOAD + 32 + 32 * NEPI;   // + 1 MMA + 8 epilogue warps
 constexpr int MAXASLOT = 4;             // TMEM A ring: up to 4 slots of 2 KC columns (hi | lo)
 constexpr uint32_t TMEM_COLS = 512;     // [0, 2 accw) double-buffered accumulators, then the A ring
 constexpr int TPITCH = 20;              // epilogue transpose buffer pitch (floats): conflict-free float4 rows
@@ -179,8 +180,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     const uint32_t ACC_COLS = 2 * (uint32_t)a.accw;
     float* eny = (float*)(bring + (size_t)MAXASLOT * b_slot);         // [NCB] ||ỹ||^2 (epilogue)
     uint32_t* eyid = (uint32_t*)(eny + NCB);                        // [NCB] query vocab ids (epilogue)
-    float* tstage = (float*)(eyid + NCB);                           // [4 warps][32][TPITCH] epilogue transpose
-    uint64_t* bars = (uint64_t*)(tstage + 4 * 32 * TPITCH);
+    float* tstage = (float*)(eyid + NCB);                           // [NEPI warps][32][TPITCH] epilogue transpose
+    uint64_t* bars = (uint64_t*)(tstage + NEPI * 32 * TPITCH);
     uint64_t* rawf = bars;                  // [Q] raw chunk landed (copy threads, noinc)
     uint64_t* remp = rawf + a.Q;            // [Q] raw slot read (converter warps)
     uint64_t* full = remp + a.Q;            // [NASLOT] A slot written + B landed
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     if (t == 0) {
         for (int q = 0; q < a.Q; q++) { mbar_init(&rawf[q], NCOPY); mbar_init(&remp[q], NCONV / 32); }
         for (int s = 0; s < NASLOT; s++) { mbar_init(&full[s], NCONV / 32 + 1); mbar_init(&aemp[s], 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], TM); }
+        for (int b = 0; b < 2; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], 32 * NEPI); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == MMA_WARP) {
@@ -357,8 +358,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
         // ------------------------------------------------------------------ epilogue
         const int quarter = warp & 3;                 // TMEM lanes 32*quarter .. +31
         const int r = quarter * 32 + lane;
-        const int et = t - (NLOAD + 32);              // 0..127 within the epilogue warps
-        float* tbuf = tstage + (size_t)(warp - MMA_WARP - 1) * 32 * TPITCH;   // this warp's 32x16 transpose buffer
+        const int ew = warp - MMA_WARP - 1;           // 0..NEPI-1
+        const int half = ew >> 2;                     // which alternate 16-column blocks this warp takes
+        const int et = t - (NLOAD + 32);              // 0..32*NEPI-1 within the epilogue warps
+        float* tbuf = tstage + (size_t)ew * 32 * TPITCH;   // this warp's 32x16 transpose buffer
         int k = 0, cur_q = -1, nb = 0;
         int64_t rb = 0;
         // next tile's descriptor, row id and row norm, loaded one tile ahead
@@ -386,13 +389,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                 const int sq = hdr->err ? 0 : (int)hdr->s;
                 nb = min(NCB, max(0, sq - a.cb * NCB));
                 rb = a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
                 const uint2* qitems = (const uint2*)(slot + a.L.off_items);
-                for (int j = et; j < NCB; j += 128) {
+                for (int j = et; j < NCB; j += 32 * NEPI) {
                     eyid[j] = j < nb ? (qitems[a.cb * NCB + j].x & FTI_VOCAB_MASK) : 0xFFFFFFFFu;
                     eny[j] = a.ny[(int64_t)q * NCB + j];
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
                 cur_q = q;
             }
             // rows of this warp: tile row 32*quarter + i; the table rows are contiguous
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
             TW(0, mbar_wait(&accf[b], (k >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.accw);
-            for (int c0 = 0; c0 < np; c0 += 16) {
+            for (int c0 = 16 * half; c0 < np; c0 += 32) {
                 uint32_t v[16], vl[16];
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
@@ -724,7 +727,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     // shared memory: Q raw slots, NASLOT B slots, epilogue staging, barriers
     const size_t raw_bytes = (size_t)TM * RPITCH;
     const size_t b_slot = 2 * (size_t)a.NPmax * KC * 4;
-    const size_t fixed = 2 * NCB * 4 + 4 * 32 * TPITCH * 4 + 512;
+    const size_t fixed = 2 * NCB * 4 + NEPI * 32 * TPITCH * 4 + 512;
     a.accw = 2 * a.NPmax;
     a.naslot = std::min(MAXASLOT, (int)(TMEM_COLS - 2 * a.accw) / (2 * KC));
     if (a.naslot < 2) return cudaErrorInvalidConfiguration;
