@@ -316,8 +316,9 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
 // test, no posting search.  The node's depth rides in the doc record (mass | depth << 16).
 __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* __restrict__ bits,
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
-                                              const ChunkHdr& sh, int nqc) {
+                                              uint2* __restrict__ hq, const ChunkHdr& sh, int nqc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
@@ -341,29 +342,31 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
         };
         for (uint32_t rb = r0; rb < r1; rb += 32) {
             const uint32_t r = rb + lane;
-            uint2 rec = make_uint2(0u, 0u);
             int id = -1;
+            uint32_t y = 0;
             if (r < r1) {
-                rec = a.qt[r];
+                const uint2 rec = a.qt[r];
+                y = rec.y;
                 const uint32_t bw = bits[rec.x >> 5], bpos = rec.x & 31u;
                 if ((bw >> bpos) & 1u) id = (int)(rank[rec.x >> 5] + __popc(bw & ((1u << bpos) - 1u)));
             }
-            unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
-            while (hm) {
-                const int l1 = __ffs(hm) - 1;
-                hm &= hm - 1;
-                const int l2 = hm ? __ffs(hm) - 1 : l1;
-                const bool two = hm != 0u;
-                hm &= hm - 1;
-                const int id1 = __shfl_sync(0xffffffffu, id, l1);
-                const uint32_t y1 = __shfl_sync(0xffffffffu, rec.y, l1);
-                const int id2 = __shfl_sync(0xffffffffu, id, l2);
-                const uint32_t y2 = __shfl_sync(0xffffffffu, rec.y, l2);
-                const uint32_t p1 = post[id1 * QT_QC + lane];
-                const uint32_t p2 = two ? (uint32_t)post[id2 * QT_QC + lane] : 0u;
-                term(p1, y1);
-                term(p2, y2);
+            // compact the batch's hits into the warp's queue, then visit them two at a time with
+            // broadcast loads (every lane reads the same {union id, mass | depth << 16})
+            const unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
+            const int nh = __popc(hm);
+            if (id >= 0) hq[__popc(hm & lt)] = make_uint2((uint32_t)id, y);
+            if (nh & 1) {
+                if (lane == 0) hq[nh] = make_uint2(0u, 0u);      // pad: mass 0 contributes 0
             }
+            __syncwarp();
+            for (int h = 0; h < nh; h += 2) {
+                const uint2 e1 = hq[h], e2 = hq[h + 1];
+                const uint32_t p1 = post[e1.x * QT_QC + lane];
+                const uint32_t p2 = post[e2.x * QT_QC + lane];
+                term(p1, e1.y);
+                term(p2, e2.y);
+            }
+            __syncwarp();
         }
         qt_store(a, sh, nqc, dp, acc, W32, A);
     }
@@ -457,8 +460,9 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
         const uint32_t* gb = (const uint32_t*)(dsrc + sizeof(DenseHdr));
         const int nwords = 2 * a.dg.mw + (int)dh.nU * QT_QC / 2;    // bits | rank | post, contiguous
         for (int i = threadIdx.x; i < nwords; i += blockDim.x) sm[i] = gb[i];
+        uint2* hq = (uint2*)(sm + ((2 * a.dg.mw + a.dg.cap * QT_QC / 2 + 1) & ~1));   // per-warp hit queues
         __syncthreads();
-        qt_scan_dense(a, bits, rank, post, sh, (int)sh.nq);
+        qt_scan_dense(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
         return;
     }
     const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
@@ -526,7 +530,9 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
     a.err = ds->err_dev;
     const size_t smem = std::max<size_t>(4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap,
-                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 : 0);
+                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 8 +
+                                                          (size_t)QT_WARPS * 32 * 8
+                                                    : 0);
     e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int ctas_per_sm = 0;
