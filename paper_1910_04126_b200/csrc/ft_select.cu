@@ -85,22 +85,30 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
         __syncthreads();
         thr = s_thr;
     }
-    // gather every key ≤ thr (all of them when L ≤ SEL_CAP)
-    for (int64_t i0 = 0; i0 < L; i0 += blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        unsigned long long hi = 0;
-        bool sel = false;
-        if (i < L) {
-            hi = okey(v[i]);
-            sel = hi <= thr;
+    // gather every key ≤ thr (all of them when L ≤ SEL_CAP); 8 loads in flight per thread, then
+    // warp-aggregated positions
+    constexpr int GU = 8;
+    for (int64_t i0 = 0; i0 < L; i0 += (int64_t)blockDim.x * GU) {
+        double vv[GU];
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+            vv[u] = i < L ? v[i] : 0.0;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, sel);
-        int base = 0;
-        if (lane == 0 && bal) base = atomicAdd(&s_cnt, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (sel) {
-            const int pos = base + __popc(bal & ((1u << lane) - 1u));
-            if (pos < SEL_CAP) { bh[pos] = hi; bl[pos] = id ? (uint32_t)id[i] : (uint32_t)i; }
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+            const unsigned long long hi = okey(vv[u]);
+            const bool sel = i < L && hi <= thr;
+            const unsigned bal = __ballot_sync(0xffffffffu, sel);
+            if (bal == 0u) continue;
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_cnt, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (sel) {
+                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                if (pos < SEL_CAP) { bh[pos] = hi; bl[pos] = id ? (uint32_t)id[i] : (uint32_t)i; }
+            }
         }
     }
     __syncthreads();
