@@ -241,7 +241,7 @@ __device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& c
 }
 
 template <bool EXPORT>
-__global__ void __launch_bounds__(FT_WARPS * 32) k_flowtree(FtArgs a) {
+__global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int q = blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
