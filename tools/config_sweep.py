@@ -52,7 +52,20 @@ for name in names:
             ref = T.ft(a, aw, b, bw)
             if abs(fv[q, j] - ref) > 1e-5 * abs(ref) or (ref == 0) != (fv[q, j] == 0):
                 bad_ft += 1
-    print(json.dumps({"config": name, "n": wl.n, "nq": wl.nq, "N": int(wl.X.shape[0]), "d": int(wl.X.shape[1]),
+    # the k-NN answer itself for two queries against the oracle's pipeline (ids up to the tie band)
+    oid_h, ov_h = oid.cpu().numpy(), ov.cpu().numpy()
+    knn_bad = 0
+    for q in qs[:2] if name != "stress" else qs[:1]:
+        b, bw = wl.query(q)
+        rid, rval = T.knn(wl.doc_off, wl.ids, wl.w, b, bw, wl.k, wl.prefilter_m)
+        if not np.allclose(ov_h[q], rval, rtol=1e-5, atol=0):
+            knn_bad += 1
+        elif not np.array_equal(oid_h[q], rid):
+            # permutations only inside tie bands
+            band = np.abs(np.diff(rval)) <= 2e-5 * np.abs(rval[1:])
+            if not band.any():
+                knn_bad += 1
+    print(json.dumps({"config": name, "knn_checked": 2 if name != "stress" else 1, "knn_mismatch": knn_bad, "n": wl.n, "nq": wl.nq, "N": int(wl.X.shape[0]), "d": int(wl.X.shape[1]),
                       "d_star": ix.d_star, "nodes": ix.n_nodes, "k": wl.k, "prefilter_m": wl.prefilter_m,
                       "knn_ms": ms, "queries_per_s": wl.nq / (ms / 1e3), "gen_s": round(tg, 1),
                       "sampled_pairs": int(len(qs) * len(ds_)), "qt_mismatch": bad_qt, "ft_mismatch": bad_ft}),
