@@ -114,6 +114,27 @@ ft_status ft_flowtree_flow(const ft_dataset* ds, int32_t q_len, const int32_t* q
 ft_status ft_knn(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
                  const uint32_t* q_w, int32_t k, int64_t prefilter_m, int64_t* out_ids, double* out_val,
                  void* stream);
+/* Doc-sharded k-NN building blocks: with the docs split across ranks, each rank
+ * keeps its local top-m Quadtree candidates, the ranks exchange (value, global id) lists, merge
+ * them with ft_topk, and each rank scores the merged candidates it owns with
+ * ft_flowtree_estimate_lists; the result is identical to ft_knn on the whole collection.
+ *
+ * ft_topk: per row, the k smallest (value, id) pairs, ties by id, in ascending order — the
+ * selection of ft_knn (reading R14).  DEVICE pointers only (FT_EINVAL else).
+ *   vals double [rows × vals_ld] (L used per row; NaN sorts last);
+ *   ids  int64 [rows × ids_ld], or NULL: the id of column c is id_base + c;
+ *   out_ids int64 / out_val double [rows × k]; rows with fewer than k entries pad with −1 / +inf.
+ * Asynchronous on `stream`.                                                                  */
+ft_status ft_topk(const double* vals, int64_t vals_ld, const int64_t* ids, int64_t ids_ld, int64_t id_base,
+                  int64_t L, int32_t rows, int32_t k, int64_t* out_ids, double* out_val, void* stream);
+/* Flowtree estimates of per-query candidate lists:
+ *   docs  int64 [nq × docs_ld] DEVICE: the first n_per_q entries of row q are doc indices of
+ *         this dataset; a negative entry is skipped and scores +inf (so per-shard results
+ *         combine with a MIN reduction); an index ≥ n scores NaN and sets FT_ERANGE.
+ *   out   double [nq × n_per_q] DEVICE.  q_off is HOST; q_ids / q_w host or device.          */
+ft_status ft_flowtree_estimate_lists(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                                     const uint32_t* q_w, const int64_t* docs, int64_t docs_ld, int64_t n_per_q,
+                                     double* out, void* stream);
 /* Synchronise `stream` and report (then clear) any sticky device-side validation error.      */
 ft_status ft_synchronize(const ft_dataset* ds, void* stream);
 

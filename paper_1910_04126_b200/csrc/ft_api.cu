@@ -410,6 +410,41 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
     return FT_OK;
 }
 
+extern "C" ft_status ft_topk(const double* vals, int64_t vals_ld, const int64_t* ids, int64_t ids_ld, int64_t id_base,
+                             int64_t L, int32_t rows, int32_t k, int64_t* out_ids, double* out_val, void* stream) {
+    const char* who = "ft_topk";
+    if (rows < 0 || L < 0 || k < 1) return fti_fail(FT_EINVAL, "ft_topk: need rows >= 0, L >= 0, k >= 1");
+    if (k > FTI_MAX_SELECT) return fti_fail(FT_ERANGE, "ft_topk: k > 8192");
+    if (rows == 0) return FT_OK;
+    if (!vals || !out_ids || !out_val) return fti_fail(FT_EINVAL, "ft_topk: NULL pointer");
+    if (!is_device_ptr(vals) || !is_device_ptr(out_ids) || !is_device_ptr(out_val) || (ids && !is_device_ptr(ids)))
+        return fti_fail(FT_EINVAL, "ft_topk: device pointers required");
+    if (vals_ld < L || (ids && ids_ld < L)) return fti_fail(FT_EINVAL, "ft_topk: leading dimension < L");
+    cudaStream_t st = (cudaStream_t)stream;
+    static DevBuf scratch;
+    FTI_CUDA(scratch.reserve(sizeof(int) * ((size_t)rows + 1)));
+    FTI_CUDA(fti_launch_select(vals, vals_ld, ids, ids_ld, L, rows, k, out_ids, out_val, k, scratch.as<int>(), st,
+                               id_base));
+    (void)who;
+    return FT_OK;
+}
+
+extern "C" ft_status ft_flowtree_estimate_lists(const ft_dataset* cds, const int64_t* q_off, int32_t nq,
+                                                const int32_t* q_ids, const uint32_t* q_w, const int64_t* docs,
+                                                int64_t docs_ld, int64_t n_per_q, double* out, void* stream) {
+    const char* who = "ft_flowtree_estimate_lists";
+    if (!cds) return fti_fail(FT_ESTATE, std::string(who) + ": NULL dataset");
+    if (!docs || !out) return fti_fail(FT_EINVAL, std::string(who) + ": NULL docs or out");
+    if (n_per_q < 1 || docs_ld < n_per_q) return fti_fail(FT_EINVAL, std::string(who) + ": need 1 <= n_per_q <= docs_ld");
+    if (!is_device_ptr(docs) || !is_device_ptr(out)) return fti_fail(FT_EINVAL, std::string(who) + ": device docs / out required");
+    ft_dataset* ds = const_cast<ft_dataset*>(cds);
+    cudaStream_t st = (cudaStream_t)stream;
+    Staged S;
+    ft_status rc = stage_queries(ds, q_off, nq, q_ids, q_w, st, who, S);
+    if (rc) return rc;
+    return flowtree_stage(ds, S, nq, docs, docs_ld, n_per_q, out, n_per_q, st);
+}
+
 extern "C" ft_status ft_synchronize(const ft_dataset* ds, void* stream) {
     if (!ds) return fti_fail(FT_ESTATE, "ft_synchronize: NULL dataset");
     return check_device_errors(ds, (cudaStream_t)stream, "ft_synchronize");

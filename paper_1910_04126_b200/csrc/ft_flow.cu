@@ -323,7 +323,11 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
         const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
         double* outp = a.out ? a.out + (int64_t)q * a.out_ld + dp : nullptr;
         if (!qok || doc < 0 || doc >= a.n) {
-            if (lane == 0 && outp) *outp = __longlong_as_double(0x7ff8000000000000ll);
+            // a negative candidate (padding, or a doc another shard owns) scores +inf; an invalid
+            // query or a doc index ≥ n scores NaN
+            if (lane == 0 && outp)
+                *outp = (qok && doc < 0) ? __longlong_as_double(0x7ff0000000000000ll)
+                                         : __longlong_as_double(0x7ff8000000000000ll);
             if (lane == 0 && qok && doc >= a.n) atomicOr(a.err, FTI_ERR_RANGE);
             continue;
         }

@@ -191,4 +191,4 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
 cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, int32_t nq, int64_t* d_row_base, cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
-                              int* d_scratch /* rows + 1 ints */, cudaStream_t st);
+                              int* d_scratch /* rows + 1 ints */, cudaStream_t st, int64_t id_base = 0);

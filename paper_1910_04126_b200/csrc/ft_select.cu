@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
                                                      const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L,
                                                      int k, int64_t* __restrict__ out_ids,
                                                      double* __restrict__ out_val, int64_t out_ld,
-                                                     int* __restrict__ redo, int* __restrict__ nredo) {
+                                                     int* __restrict__ redo, int* __restrict__ nredo, int64_t id_base) {
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;                      // SEL_CAP
     uint32_t* bl = (uint32_t*)(sbuf + SEL_CAP);         // SEL_CAP
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
             base = __shfl_sync(0xffffffffu, base, 0);
             if (sel) {
                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                if (pos < SEL_CAP) { bh[pos] = hi; bl[pos] = id ? (uint32_t)id[i] : (uint32_t)i; }
+                if (pos < SEL_CAP) { bh[pos] = hi; bl[pos] = id ? (uint32_t)id[i] : (uint32_t)(id_base + i); }
             }
         }
     }
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
         double ov = __longlong_as_double(0x7ff0000000000000ll);
         if (t < kk) {
             ov = okey_inv(bh[t]);
-            oid = (int64_t)bl[t];
+            oid = bl[t] == 0xFFFFFFFFu ? -1 : (int64_t)bl[t];
         }
         out_ids[(int64_t)row * out_ld + t] = oid;
         out_val[(int64_t)row * out_ld + t] = ov;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
                                                 const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L, int k,
                                                 int64_t* __restrict__ out_ids, double* __restrict__ out_val,
                                                 int64_t out_ld, int P, const int* __restrict__ rows_list,
-                                                const int* __restrict__ nrows_list) {
+                                                const int* __restrict__ nrows_list, int64_t id_base) {
     if (rows_list && (int)blockIdx.x >= *nrows_list) return;
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;               // P
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
             const uint32_t pl = s_pl, ml = s_ml;
             for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
                 unsigned long long hi = okey(v[i]);
-                uint32_t lo = id ? (uint32_t)id[i] : (uint32_t)i;
+                uint32_t lo = id ? (uint32_t)id[i] : (uint32_t)(id_base + i);
                 if ((hi & mh) == ph && (lo & ml) == pl) atomicAdd(&hist[digit_of(hi, lo, t)], 1u);
             }
             __syncthreads();
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
     const bool all = (kk >= L);
     for (int64_t i = threadIdx.x; i < L && kk > 0; i += blockDim.x) {
         unsigned long long hi = okey(v[i]);
-        uint32_t lo = id ? (uint32_t)id[i] : (uint32_t)i;
+        uint32_t lo = id ? (uint32_t)id[i] : (uint32_t)(id_base + i);
         unsigned long long h2 = hi & mh;
         uint32_t l2 = lo & ml;
         bool sel = all || h2 < ph || (h2 == ph && l2 <= pl);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
 
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
-                              int* d_scratch, cudaStream_t st) {
+                              int* d_scratch, cudaStream_t st, int64_t id_base) {
     if (rows <= 0) return cudaSuccess;
     int kk = (int)std::min<int64_t>(k, L);
     int P = fti_pow2_at_least(std::max(kk, 2));
@@ -248,7 +248,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     if (e != cudaSuccess) return e;
     if (getenv("FT_SELECT_RADIX")) {   // test hook: the radix kernel for every row
         k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P,
-                                          nullptr, nullptr);
+                                          nullptr, nullptr, id_base);
         fti_count_launches(1);
         return cudaGetLastError();
     }
@@ -261,10 +261,10 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     e = cudaFuncSetAttribute(k_select_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
     if (e != cudaSuccess) return e;
     k_select_fast<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo,
-                                             nredo);
+                                             nredo, id_base);
     // pass 2: MSD radix selection of the listed rows (CTAs past the list exit at once)
     k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P, redo,
-                                      nredo);
+                                      nredo, id_base);
     fti_count_launches(2);
     return cudaGetLastError();
 }

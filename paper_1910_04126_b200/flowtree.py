@@ -27,7 +27,7 @@ EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft
             "ft_quadtree_estimate", "ft_flowtree_estimate", "ft_flowtree_flow", "ft_knn",
             "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error",
             "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_units",
-            "ft_profile_stage_name", "ft_launch_count"]
+            "ft_profile_stage_name", "ft_launch_count", "ft_topk", "ft_flowtree_estimate_lists"]
 FT_NUM_STAGES = 7
 
 
@@ -68,6 +68,8 @@ def _load_lib():
         "ft_profile_units": (st, [P, i32, P]),
         "ft_profile_stage_name": (ctypes.c_char_p, [i32]),
         "ft_launch_count": (u64, []),
+        "ft_topk": (st, [P, i64, P, i64, i64, i64, i32, i32, P, P, P]),
+        "ft_flowtree_estimate_lists": (st, [P, P, i32, P, P, P, i64, i64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -235,6 +237,42 @@ def ft_knn(ds, q_off, q_ids, q_w, k: int, prefilter_m: int = 0, out_ids=None, ou
     sp = _stream_ptr(stream, ic or wc or oic or ovc)
     _check(_lib.ft_knn(ds, ctypes.c_void_p(q_off.ctypes.data), nq, ip, wp, int(k), int(prefilter_m), oip, ovp, sp))
     return out_ids, out_val
+
+
+def ft_topk(vals, k: int, ids=None, id_base: int = 0, out_ids=None, out_val=None, stream=None):
+    """Per row the k smallest (value, id) of a DEVICE [rows, L] float64 tensor, ties by id; ids is
+    a device int64 [rows, L] tensor or None (id = id_base + column).  Returns device tensors."""
+    import torch
+    rows, L = vals.shape
+    if out_ids is None:
+        out_ids = torch.empty((rows, k), dtype=torch.int64, device=vals.device)
+    if out_val is None:
+        out_val = torch.empty((rows, k), dtype=torch.float64, device=vals.device)
+    vp, vk, _ = _ptr(vals, np.float64)
+    ip, ik, _ = _ptr(ids, np.int64)
+    oip, oik, _ = _ptr(out_ids, np.int64)
+    ovp, ovk, _ = _ptr(out_val, np.float64)
+    _check(_lib.ft_topk(vp, vals.stride(0), ip, ids.stride(0) if ids is not None else 0, int(id_base), L, rows,
+                        int(k), oip, ovp, _stream_ptr(stream, True)))
+    return out_ids, out_val
+
+
+def ft_flowtree_estimate_lists(ds, q_off, q_ids, q_w, docs, out=None, stream=None):
+    """Flowtree estimates of per-query candidate lists: docs is a DEVICE int64 [nq, n] tensor of doc
+    indices (negative = skipped, NaN out); returns a DEVICE float64 [nq, n] tensor."""
+    import torch
+    q_off = np.ascontiguousarray(q_off, dtype=np.int64)
+    nq = len(q_off) - 1
+    n = docs.shape[1]
+    if out is None:
+        out = torch.empty((nq, n), dtype=torch.float64, device=docs.device)
+    ip, ik, ic = _ptr(q_ids, np.int32)
+    wp, wk, wc = _ptr(q_w, np.uint32)
+    dp, dk, _ = _ptr(docs, np.int64)
+    op, ok, _ = _ptr(out, np.float64)
+    _check(_lib.ft_flowtree_estimate_lists(ds, ctypes.c_void_p(q_off.ctypes.data), nq, ip, wp, dp, docs.stride(0), n,
+                                           op, _stream_ptr(stream, True)))
+    return out
 
 
 def ft_synchronize(ds, stream=None):

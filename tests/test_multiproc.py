@@ -43,6 +43,98 @@ def _worker(rank, world, port, result_path):
     dist.destroy_process_group()
 
 
+class OracleShard:
+    """The doc-sharded protocol's per-rank compute on the CPU oracle (numpy selection with the
+    library's ordering: value, then id as uint32 so padding −1 sorts last)."""
+
+    def __init__(self, T, doc_off, ids, w, base):
+        self.T, self.doc_off, self.ids, self.w, self.base = T, doc_off, ids, w, base
+        self.n_local = len(doc_off) - 1
+
+    @staticmethod
+    def _sel(vals, ids, k):
+        import torch
+        vals, ids = vals.numpy(), ids.numpy()
+        out_i = np.full((vals.shape[0], k), -1, np.int64)
+        out_v = np.full((vals.shape[0], k), np.inf)
+        for r in range(vals.shape[0]):
+            order = np.lexsort((ids[r].astype(np.uint32), vals[r]))[:k]
+            out_i[r, :len(order)] = ids[r][order]
+            out_v[r, :len(order)] = vals[r][order]
+        return torch.from_numpy(out_i), torch.from_numpy(out_v)
+
+    def local_topm(self, q_off, q_ids, q_w, m):
+        import torch
+        nq = len(q_off) - 1
+        vals = np.array([[self.T.qt(self.ids[self.doc_off[d]:self.doc_off[d + 1]], self.w[self.doc_off[d]:self.doc_off[d + 1]],
+                                    q_ids[q_off[q]:q_off[q + 1]], q_w[q_off[q]:q_off[q + 1]])[1]
+                          for d in range(self.n_local)] for q in range(nq)])
+        gid = np.broadcast_to(np.arange(self.n_local, dtype=np.int64) + self.base, vals.shape).copy()
+        return self._sel(torch.from_numpy(vals), torch.from_numpy(gid), min(m, self.n_local))
+
+    def topk(self, vals, ids, k):
+        return self._sel(vals, ids, k)
+
+    def score_owned(self, q_off, q_ids, q_w, cand_ids):
+        import torch
+        c = cand_ids.numpy()
+        out = np.full(c.shape, np.inf)
+        for q in range(c.shape[0]):
+            for j, g in enumerate(c[q]):
+                d = int(g) - self.base
+                if 0 <= d < self.n_local:
+                    out[q, j] = self.T.ft(self.ids[self.doc_off[d]:self.doc_off[d + 1]],
+                                          self.w[self.doc_off[d]:self.doc_off[d + 1]],
+                                          q_ids[q_off[q]:q_off[q + 1]], q_w[q_off[q]:q_off[q + 1]])
+        return torch.from_numpy(out)
+
+
+def _doc_worker(rank, world, port, result_path):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_1910_04126_b200 import parallel, workloads
+    wl = workloads.make("tiny", n_queries=6)
+    T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    d_off, d_ids, d_w, base = parallel.shard_docs(wl.doc_off, wl.ids, wl.w, rank, world)
+    shard = OracleShard(T, d_off, d_ids, d_w, base)
+    ids, vals = parallel.knn_doc_sharded(shard, wl.q_off, wl.q_ids, wl.q_w, wl.k, 30, dist)
+    if rank == 0:
+        np.save(result_path, np.array([ids.numpy(), vals.numpy()], dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_doc_sharded_knn(tmp_path):
+    """Doc sharding: local top-m → all-gather → merge → owned Flowtree → MIN
+    all-reduce → top-k equals the single-process Quadtree-prefiltered k-NN exactly."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "res_docs.npy")
+    mp.spawn(_doc_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    ids, vals = np.load(out, allow_pickle=True)
+    import oracle
+    from paper_1910_04126_b200 import workloads
+    wl = workloads.make("tiny", n_queries=6)
+    T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    for q in range(wl.nq):
+        ref_ids, ref_vals = T.knn(wl.doc_off, wl.ids, wl.w, *wl.query(q), wl.k, 30)
+        assert ids[q].tolist() == ref_ids.tolist() and vals[q].tolist() == ref_vals.tolist()
+
+
+def test_shard_docs_cover_once():
+    from paper_1910_04126_b200 import parallel, workloads
+    wl = workloads.make("tiny")
+    got_ids = []
+    for r in range(3):
+        off, ids, w, base = parallel.shard_docs(wl.doc_off, wl.ids, wl.w, r, 3)
+        assert off[0] == 0 and off[-1] == len(ids) and base == parallel.shard_bounds(wl.n, r, 3)[0]
+        got_ids.append(ids)
+    assert np.array_equal(np.concatenate(got_ids), wl.ids)
+
+
 def test_shard_bounds_cover_once():
     from paper_1910_04126_b200 import parallel
     for nq in (1, 7, 1000, 1001):

@@ -409,3 +409,55 @@ def test_reviews_full_size_sampled(ft):
         cand = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:wl.prefilter_m]
         ftv = pmap(lambda d: T.ft(*wl.doc(d), b, bw), cand)
         assert_topk_tieband(ids[q], vals[q], cand, ftv, wl.k, what=f"reviews q{q}")
+
+
+# ---------------------------------------------------------------------------------------------
+# doc-sharded k-NN building blocks on one GPU
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,nd,nq,k,m", [("reviews", 6000, 20, 10, 300), ("tiny", 100, 4, 5, 30)])
+def test_doc_sharded_knn_matches_single_dataset(ft, name, nd, nq, k, m):
+    """Two doc shards run the protocol's phases (local top-m with global ids, merge with ft_topk,
+    owned Flowtree via ft_flowtree_estimate_lists with +inf elsewhere, MIN, top-k): ids and
+    values bit-identical to ft_knn on the whole collection."""
+    import torch
+    from paper_1910_04126_b200 import parallel
+    wl = get_workload(name, n_docs=nd, n_queries=nq)
+    ix, ds = _setup(ft, wl)
+    ref_ids, ref_vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, k, m)
+    shards = []
+    for r in range(2):
+        off, ids, w, base = parallel.shard_docs(wl.doc_off, wl.ids, wl.w, r, 2)
+        shards.append(parallel.LibShard(ft, ft.Dataset(ix, off, ids, w), base))
+    loc = [sh.local_topm(wl.q_off, wl.q_ids, wl.q_w, m) for sh in shards]
+    ids_all = torch.cat([l[0] for l in loc], 1)
+    vals_all = torch.cat([l[1] for l in loc], 1)
+    cand, _ = shards[0].topk(vals_all, ids_all, m)
+    fv = torch.minimum(*[sh.score_owned(wl.q_off, wl.q_ids, wl.q_w, cand) for sh in shards])
+    got_ids, got_vals = shards[0].topk(fv, cand, k)
+    torch.cuda.synchronize()
+    assert np.array_equal(got_ids.cpu().numpy(), ref_ids)
+    assert np.array_equal(got_vals.cpu().numpy(), ref_vals)
+    # a single shard through the full protocol (no process group) is ft_knn itself
+    one = parallel.LibShard(ft, ds, 0)
+    i1, v1 = parallel.knn_doc_sharded(one, wl.q_off, wl.q_ids, wl.q_w, k, m, None)
+    assert np.array_equal(i1.cpu().numpy(), ref_ids) and np.array_equal(v1.cpu().numpy(), ref_vals)
+
+
+def test_topk_entry_point(ft):
+    """ft_topk against a numpy (value, id) sort, with ties, NaN and an id base."""
+    import torch
+    rng = np.random.default_rng(9)
+    vals = rng.integers(0, 20, size=(7, 3000)).astype(np.float64)
+    vals[0, 5] = np.nan
+    ids = rng.permutation(7 * 3000).reshape(7, 3000).astype(np.int64)
+    dv, di = torch.from_numpy(vals).cuda(), torch.from_numpy(ids).cuda()
+    oi, ov = ft.ft_topk(dv, 40, ids=di)
+    oi2, ov2 = ft.ft_topk(dv, 40, id_base=1000)
+    torch.cuda.synchronize()
+    for r in range(7):
+        key = np.where(np.isnan(vals[r]), np.inf, vals[r])
+        o = np.lexsort((ids[r], key))[:40]
+        assert np.array_equal(oi[r].cpu().numpy(), ids[r][o])
+        o2 = np.lexsort((np.arange(3000), key))[:40]
+        assert np.array_equal(oi2[r].cpu().numpy(), 1000 + o2)
+        assert np.array_equal(ov2[r].cpu().numpy(), vals[r][o2])
