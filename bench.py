@@ -7,9 +7,11 @@ ft_knn(queries, k=10, prefilter_m=1000) = query prep → Quadtree over all n=100
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Multi-GPU (torchrun, one process per GPU): every rank holds the dataset and answers its own
-batch of queries — the path shards by query with no data-path collective, so
+Multi-GPU (torchrun, one process per GPU): by default every rank holds the dataset and answers its
+own batch of queries — the path shards by query with no data-path collective, so
 scaling is weak; the device time is the max over ranks (NCCL all-reduce of the timings only).
+--shard docs splits the docs instead: every rank answers the whole batch over its
+doc range and the ranks exchange top-m candidate lists over NCCL (strong scaling).
 Prints one JSON line on rank 0.  --impl reference times the CPU oracle (the only other place
 this file runs oracle/) on the same config, metric and unit.
 """
@@ -159,15 +161,24 @@ def run_b200(args):
     from paper_1910_04126_b200 import flowtree as ft, parallel, workloads
 
     Q = args.queries
-    wl_all = workloads.make(CONFIG, n_queries=Q * world)
-    q_off, q_ids_h, q_w_h, _ = parallel.shard_queries(wl_all.q_off, wl_all.q_ids, wl_all.q_w, rank, world)
+    docs_mode = args.shard == "docs"
+    wl_all = workloads.make(CONFIG, n_queries=Q if docs_mode else Q * world)
+    if docs_mode:
+        q_off, q_ids_h, q_w_h = wl_all.q_off, wl_all.q_ids, wl_all.q_w
+    else:
+        q_off, q_ids_h, q_w_h, _ = parallel.shard_queries(wl_all.q_off, wl_all.q_ids, wl_all.q_w, rank, world)
     wl = wl_all
     k, m = wl.k, wl.prefilter_m
 
     t_build = time.perf_counter()
     ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
     t_load = time.perf_counter()
-    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    if docs_mode:
+        d_off, d_ids, d_w, d_base = parallel.shard_docs(wl.doc_off, wl.ids, wl.w, rank, world)
+        ds = ft.Dataset(ix, d_off, d_ids, d_w)
+        shard = parallel.LibShard(ft, ds, d_base)
+    else:
+        ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
     t_done = time.perf_counter()
     build_s, load_s = t_load - t_build, t_done - t_load
 
@@ -179,7 +190,10 @@ def run_b200(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        ds.knn(q_off, q_ids, q_w, k, m, out_ids=out_ids, out_val=out_val, stream=stream)
+        if docs_mode:
+            parallel.knn_doc_sharded(shard, q_off, q_ids, q_w, k, m, dist)
+        else:
+            ds.knn(q_off, q_ids, q_w, k, m, out_ids=out_ids, out_val=out_val, stream=stream)
 
     def barrier_sync():
         torch.cuda.synchronize()
@@ -210,7 +224,8 @@ def run_b200(args):
     units = {"dist_table": ft.ft_profile_units(ds.h, 4), "flowtree": ft.ft_profile_units(ds.h, 5)}
     ft.ft_profile_enable(ds.h, False)
     t_ms = parallel.max_over_ranks(t_ms, dist, dev)
-    value = world * Q * args.steps / (t_ms / 1e3)
+    jobq = Q if docs_mode else world * Q                 # queries the whole job answers per step
+    value = jobq * args.steps / (t_ms / 1e3)
 
     # ---- live roofline of the step's kernels; `roofline` is the dominant one (largest device time) ----
     # algorithmic bytes (SURVEY §8(d) and DESIGN.md §7): Quadtree 8 B per doc tree node + 16 B per doc
@@ -290,15 +305,23 @@ def run_b200(args):
     qw_pin = torch.from_numpy(q_w_h.view(np.int32).copy()).pin_memory().view(torch.uint32)
     oi_pin = torch.empty((Q, k), dtype=torch.int64).pin_memory()
     ov_pin = torch.empty((Q, k), dtype=torch.float64).pin_memory()
+    def e2e_step():
+        if docs_mode:
+            ri, rv = parallel.knn_doc_sharded(shard, q_off, qi_pin, qw_pin, k, m, dist)
+            oi_pin.copy_(ri, non_blocking=True)
+            ov_pin.copy_(rv, non_blocking=True)
+        else:
+            ds.knn(q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream)
+
     for _ in range(2):
-        ds.knn(q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream)
+        e2e_step()
     barrier_sync()
     e_ms = 0.0
     for i in range(args.steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ds.knn(q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream)
+        e2e_step()
         e1.record(stream)
         e1.synchronize()
         e_ms += e0.elapsed_time(e1)
@@ -306,7 +329,7 @@ def run_b200(args):
     e_ms = parallel.max_over_ranks(e_ms, dist, dev)
     h2d = 8 * (Q + 1) + 4 * len(q_ids_h) + 4 * len(q_w_h)
     d2h = Q * k * (8 + 8)
-    e2e = {"value": world * Q * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+    e2e = {"value": jobq * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h}
 
     # ---- CPU baseline: the oracle, rank 0 at N=1 only, bounded sample ----
@@ -324,11 +347,13 @@ def run_b200(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if docs_mode else "weak",
             "vs_baseline": None, "dtype": "u64/f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n": ds.n, "N": wl.X.shape[0], "d": wl.X.shape[1],
-                       "queries_per_rank": Q, "global_batch": Q * world, "k": k, "prefilter_m": m,
-                       "parallelism": f"query-sharded x{world}", "l2": "flushed (512 MiB write) between timed steps",
+                       "queries_per_rank": Q, "global_batch": jobq, "k": k, "prefilter_m": m,
+                       "parallelism": f"{'doc' if docs_mode else 'query'}-sharded x{world}",
+                       "l2": "flushed (512 MiB write) between timed steps",
                        "qt_records": int(n_qt), "nnz": int(ds.nnz)},
             "ft_estimates_per_s": kernels.get("flowtree_all_docs", {}).get("pairs_per_s"),
             "qt_estimates_per_s": kernels.get("quadtree_all_docs", {}).get("pairs_per_s"),
@@ -354,6 +379,8 @@ def main():
     p.add_argument("--ft-queries", type=int, default=64, help="queries for the exhaustive Flowtree kernel line")
     p.add_argument("--no-kernels", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--shard", default="queries", choices=["queries", "docs"],
+                   help="multi-GPU layout: replicate docs and split queries (weak), or split docs (strong)")
     args = p.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
