@@ -135,6 +135,15 @@ ft_status ft_topk(const double* vals, int64_t vals_ld, const int64_t* ids, int64
 ft_status ft_flowtree_estimate_lists(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
                                      const uint32_t* q_w, const int64_t* docs, int64_t docs_ld, int64_t n_per_q,
                                      double* out, void* stream);
+/* Exact W1 (Eq. (1)) of per-query candidate lists — the last stage of the
+ * paper's Quadtree → Flowtree → Exact pipelines: the transportation simplex
+ * on the cross-scaled integer masses, FP32 Euclidean costs, FP64 objective, one CTA per pair.
+ * Same layout as ft_flowtree_estimate_lists (DEVICE docs [nq × docs_ld], out [nq × n_per_q];
+ * negative entries score +inf).  Supports are limited to 128 points per side (larger pairs:
+ * NaN + FT_ERANGE via ft_synchronize); a pivot cap guards against cycling (NaN likewise).     */
+ft_status ft_exact_w1_lists(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                            const uint32_t* q_w, const int64_t* docs, int64_t docs_ld, int64_t n_per_q, double* out,
+                            void* stream);
 /* Synchronise `stream` and report (then clear) any sticky device-side validation error.      */
 ft_status ft_synchronize(const ft_dataset* ds, void* stream);
 

@@ -16,6 +16,9 @@ citations are in the C file's header.  Parity status of each function (DESIGN.md
   numerator, LP tree-optimality, Flowtree ≥ exact W1 (Birkhoff brute force / LP), the hand-worked
   tie-break example (golden), and the random-model isolation case (Flowtree = W1).
 * ``knn`` (O10): pinned against a full Python sort by (value, id).
+* ``exact_w1`` (O11): W1 of Eq. (1) as the transportation LP (scipy HiGHS, FP64 costs) on the
+  cross-scaled integer masses; pinned by the Birkhoff permutation brute force on uniform
+  equal-size supports and the 1-D CDF closed form (tests/test_oracle_pins.py).
 """
 from __future__ import annotations
 
@@ -194,6 +197,31 @@ class Tree:
         if rc != OR_OK:
             raise OracleError(rc, "knn")
         return out_ids, out_val
+
+
+def exact_w1(X, mu_ids, mu_w, nu_ids, nu_w) -> float:
+    """O11 — W1(μ, ν) of PAPER.md:21-26 (Eq. (1)): min Σ τ_ij ‖x_i − y_j‖ over transport plans τ
+    with marginals μ, ν.  Solved as the transportation LP on the cross-scaled integer masses
+    (a_i = w_i U, b_j = u_j W, divided by W U at the end; reading R13), FP64 costs, by scipy's
+    HiGHS (a library LP solver as the step, no other arithmetic)."""
+    from scipy.optimize import linprog
+    Xd = np.asarray(X, np.float64)
+    mu_ids = np.asarray(mu_ids, np.int64); nu_ids = np.asarray(nu_ids, np.int64)
+    w = np.asarray(mu_w, np.float64); u = np.asarray(nu_w, np.float64)
+    W, U = w.sum(), u.sum()
+    a, b = w * U, u * W
+    C = np.sqrt(((Xd[mu_ids][:, None, :] - Xd[nu_ids][None, :, :]) ** 2).sum(-1))
+    p, q = C.shape
+    A_eq = np.zeros((p + q, p * q))
+    for i in range(p):
+        A_eq[i, i * q:(i + 1) * q] = 1.0
+    for j in range(q):
+        A_eq[p + j, j::q] = 1.0
+    res = linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([a, b]), bounds=(0, None), method="highs",
+                  options={"primal_feasibility_tolerance": 1e-10, "dual_feasibility_tolerance": 1e-10})
+    if res.status != 0:
+        raise OracleError(-1, "exact_w1: " + res.message)
+    return float(res.fun) / (W * U)
 
 
 def dataset_pairs(tree: Tree, doc_off, ids, w, q_off, q_ids, q_w, pairs, which="qt"):

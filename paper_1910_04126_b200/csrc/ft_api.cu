@@ -445,6 +445,23 @@ extern "C" ft_status ft_flowtree_estimate_lists(const ft_dataset* cds, const int
     return flowtree_stage(ds, S, nq, docs, docs_ld, n_per_q, out, n_per_q, st);
 }
 
+extern "C" ft_status ft_exact_w1_lists(const ft_dataset* cds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
+                                       const uint32_t* q_w, const int64_t* docs, int64_t docs_ld, int64_t n_per_q,
+                                       double* out, void* stream) {
+    const char* who = "ft_exact_w1_lists";
+    if (!cds) return fti_fail(FT_ESTATE, std::string(who) + ": NULL dataset");
+    if (!docs || !out) return fti_fail(FT_EINVAL, std::string(who) + ": NULL docs or out");
+    if (n_per_q < 1 || docs_ld < n_per_q) return fti_fail(FT_EINVAL, std::string(who) + ": need 1 <= n_per_q <= docs_ld");
+    if (!is_device_ptr(docs) || !is_device_ptr(out)) return fti_fail(FT_EINVAL, std::string(who) + ": device docs / out required");
+    ft_dataset* ds = const_cast<ft_dataset*>(cds);
+    cudaStream_t st = (cudaStream_t)stream;
+    Staged S;
+    ft_status rc = stage_queries(ds, q_off, nq, q_ids, q_w, st, who, S);
+    if (rc) return rc;
+    FTI_CUDA(fti_launch_exact(ds, S.L, S.qblock, nq, docs, docs_ld, n_per_q, out, n_per_q, st));
+    return FT_OK;
+}
+
 extern "C" ft_status ft_synchronize(const ft_dataset* ds, void* stream) {
     if (!ds) return fti_fail(FT_ESTATE, "ft_synchronize: NULL dataset");
     return check_device_errors(ds, (cudaStream_t)stream, "ft_synchronize");

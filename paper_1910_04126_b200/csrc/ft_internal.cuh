@@ -178,6 +178,10 @@ struct FtTable {
 cudaError_t fti_launch_ftx(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t n_docs,
                            const FtTable& tab, double* d_out, int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt,
                            cudaStream_t st);
+// exact W1 of per-query candidate lists by the transportation simplex (ft_exact.cu)
+cudaError_t fti_launch_exact(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                             const int64_t* d_docs, int64_t docs_ld, int64_t n_per_q, double* d_out, int64_t out_ld,
+                             cudaStream_t st);
 cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab,
                           double* d_out, int64_t out_ld, uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap,

@@ -27,7 +27,8 @@ EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft
             "ft_quadtree_estimate", "ft_flowtree_estimate", "ft_flowtree_flow", "ft_knn",
             "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error",
             "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_units",
-            "ft_profile_stage_name", "ft_launch_count", "ft_topk", "ft_flowtree_estimate_lists"]
+            "ft_profile_stage_name", "ft_launch_count", "ft_topk", "ft_flowtree_estimate_lists",
+            "ft_exact_w1_lists"]
 FT_NUM_STAGES = 7
 
 
@@ -70,6 +71,7 @@ def _load_lib():
         "ft_launch_count": (u64, []),
         "ft_topk": (st, [P, i64, P, i64, i64, i64, i32, i32, P, P, P]),
         "ft_flowtree_estimate_lists": (st, [P, P, i32, P, P, P, i64, i64, P, P]),
+        "ft_exact_w1_lists": (st, [P, P, i32, P, P, P, i64, i64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -272,6 +274,24 @@ def ft_flowtree_estimate_lists(ds, q_off, q_ids, q_w, docs, out=None, stream=Non
     op, ok, _ = _ptr(out, np.float64)
     _check(_lib.ft_flowtree_estimate_lists(ds, ctypes.c_void_p(q_off.ctypes.data), nq, ip, wp, dp, docs.stride(0), n,
                                            op, _stream_ptr(stream, True)))
+    return out
+
+
+def ft_exact_w1_lists(ds, q_off, q_ids, q_w, docs, out=None, stream=None):
+    """Exact W1 of per-query candidate lists (DEVICE int64 [nq, n] doc indices; negative =
+    skipped, +inf out); returns a DEVICE float64 [nq, n] tensor."""
+    import torch
+    q_off = np.ascontiguousarray(q_off, dtype=np.int64)
+    nq = len(q_off) - 1
+    n = docs.shape[1]
+    if out is None:
+        out = torch.empty((nq, n), dtype=torch.float64, device=docs.device)
+    ip, ik, ic = _ptr(q_ids, np.int32)
+    wp, wk, wc = _ptr(q_w, np.uint32)
+    dp, dk, _ = _ptr(docs, np.int64)
+    op, ok, _ = _ptr(out, np.float64)
+    _check(_lib.ft_exact_w1_lists(ds, ctypes.c_void_p(q_off.ctypes.data), nq, ip, wp, dp, docs.stride(0), n, op,
+                                  _stream_ptr(stream, True)))
     return out
 
 

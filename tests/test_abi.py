@@ -15,7 +15,7 @@ PKG = os.path.join(ROOT, "paper_1910_04126_b200")
 def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ft_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ft_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")

@@ -251,6 +251,25 @@ def test_exact_w1_1d_cdf():
         assert abs(cdf - H.exact_w1(X, a, aw, b, bw)) < 1e-9
 
 
+def test_oracle_exact_w1_pins(tiny):
+    """O11 (oracle.exact_w1) against the Birkhoff permutation brute force (uniform s = 8 on the
+    tiny config) and the 1-D CDF closed form with integer weights; never above Flowtree."""
+    T = oracle.Tree(tiny.X, seed=tiny.tree_seed, max_depth=tiny.max_depth)
+    for qi in range(2):
+        b, bw = tiny.query(qi)
+        for di in range(3):
+            a, aw = tiny.doc(di)
+            w1 = oracle.exact_w1(tiny.X, a, aw, b, bw)
+            assert abs(w1 - H.birkhoff_w1(tiny.X, a, b)) < 1e-9
+            assert T.ft(a, aw, b, bw) >= w1 - 1e-12
+    rng = np.random.default_rng(17)
+    for _ in range(10):
+        X = np.sort(rng.uniform(0, 10, size=9)).astype(np.float32)[:, None]
+        a = rng.choice(9, 4, replace=False); b = rng.choice(9, 3, replace=False)
+        aw = rng.integers(1, 5, size=4); bw = rng.integers(1, 5, size=3)
+        assert abs(H.w1_1d_cdf(X[a, 0], aw, X[b, 0], bw) - oracle.exact_w1(X, a, aw, b, bw)) < 1e-9
+
+
 def test_flowtree_equals_w1_when_pairs_isolated():
     """Random-model special case: if the smallest cell containing x_k also
     contains y_k and no other support point, the tree flow is the planted perfect matching and

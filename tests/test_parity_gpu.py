@@ -461,3 +461,67 @@ def test_topk_entry_point(ft):
         o2 = np.lexsort((np.arange(3000), key))[:40]
         assert np.array_equal(oi2[r].cpu().numpy(), 1000 + o2)
         assert np.array_equal(ov2[r].cpu().numpy(), vals[r][o2])
+
+
+# ---------------------------------------------------------------------------------------------
+# exact-W1 stage
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,nd,nq,per_q", [("reviews", 3000, 6, 12), ("tiny", 100, 4, 10), ("text", 800, 3, 6)])
+def test_exact_w1_matches_lp(ft, name, nd, nq, per_q):
+    """Transportation simplex per (query, doc) against the oracle's exact W1 (LP, FP64 costs):
+    within 1e-6 relative (FP32 costs); exact ≤ Flowtree; negative entries score +inf; supports
+    beyond 128 points are NaN (text has docs up to 150)."""
+    import torch
+    wl = get_workload(name, n_docs=nd, n_queries=nq)
+    ix, ds = _setup(ft, wl)
+    rng = np.random.default_rng(11)
+    docs = np.stack([rng.choice(wl.n, per_q, replace=False) for _ in range(nq)]).astype(np.int64)
+    docs[0, -1] = -1
+    d_docs = torch.from_numpy(docs).cuda()
+    ex = ft.ft_exact_w1_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, d_docs).cpu().numpy()
+    fl = ft.ft_flowtree_estimate_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, d_docs).cpu().numpy()
+    assert np.isinf(ex[0, -1]) and np.isinf(fl[0, -1])
+    checked = 0
+    over = False
+    for q in range(nq):
+        b, bw = wl.query(q)
+        for j in range(per_q):
+            d = int(docs[q, j])
+            if d < 0:
+                continue
+            a, aw = wl.doc(d)
+            if len(a) > 128 or len(b) > 128:
+                assert np.isnan(ex[q, j])
+                over = True
+                continue
+            ref = oracle.exact_w1(wl.X, a, aw, b, bw)
+            assert abs(ex[q, j] - ref) <= 1e-6 * max(ref, 1e-12), (q, d, ex[q, j], ref)
+            assert ex[q, j] <= fl[q, j] * (1 + 1e-6) + 1e-12
+            checked += 1
+    assert checked >= nq * per_q // 3
+    if over:                # the >128-point pairs set the sticky capacity error
+        with pytest.raises(ft.FlowtreeError):
+            ds.synchronize()
+    ds.synchronize()
+
+
+def test_three_stage_pipeline_matches_oracle(ft):
+    """Quadtree → Flowtree → Exact (Table 5 "424, 9, 1") against the oracle chain: the
+    oracle's QT top-c1 → FT top-c2 (oracle.knn) → exact W1 by LP → smallest; the ids agree unless
+    two survivors' W1 lie within the 1e-6 tolerance band."""
+    from paper_1910_04126_b200 import pipeline
+    wl = get_workload("reviews", n_docs=4000, n_queries=6)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    ids, w1 = pipeline.knn_qt_ft_exact(ft, ds, wl.q_off, wl.q_ids, wl.q_w, c1=424, c2=9, k=1)
+    ids, w1 = ids.cpu().numpy(), w1.cpu().numpy()
+    for q in range(wl.nq):
+        b, bw = wl.query(q)
+        surv, _ = T.knn(wl.doc_off, wl.ids, wl.w, b, bw, 9, 424)
+        ex = [oracle.exact_w1(wl.X, *wl.doc(int(d)), b, bw) for d in surv]
+        order = sorted(range(len(surv)), key=lambda i: (ex[i], surv[i]))
+        best = order[0]
+        assert abs(w1[q, 0] - ex[best]) <= 1e-6 * ex[best]
+        if ids[q, 0] != surv[best]:
+            got = list(surv).index(ids[q, 0])
+            assert abs(ex[got] - ex[best]) <= 2e-6 * ex[best]
