@@ -299,6 +299,22 @@ def run_b200(args):
             "frac_hbm": ft_bytes / (fms / 1e3) / 1e9 / peak,
             "pairs_per_s_incl_table": nqf * ds.n / ((fms + tms) / 1e3)}
         del out_ft
+        # the paper's three-stage pipeline (Table 5: Quadtree 424 -> Flowtree 9 -> Exact 1), full batch
+        from paper_1910_04126_b200 import pipeline
+        c1, c2 = min(424, ds.n), min(9, ds.n)
+        for _ in range(2):
+            pipeline.knn_qt_ft_exact(ft, ds, q_off, q_ids, q_w, c1, c2, 1, stream=stream)
+        p_ms = 0.0
+        for _ in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pipeline.knn_qt_ft_exact(ft, ds, q_off, q_ids, q_w, c1, c2, 1, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            p_ms += e0.elapsed_time(e1) / 3
+        kernels["pipeline_qt_ft_exact"] = {"c1": c1, "c2": c2, "k": 1, "queries": Q, "ms": p_ms,
+                                           "queries_per_s": Q / (p_ms / 1e3)}
 
     # ---- e2e: same metric through the C ABI with pinned HOST buffers ----
     qi_pin = torch.from_numpy(q_ids_h.copy()).pin_memory()

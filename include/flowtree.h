@@ -139,7 +139,7 @@ ft_status ft_flowtree_estimate_lists(const ft_dataset* ds, const int64_t* q_off,
  * paper's Quadtree → Flowtree → Exact pipelines: the transportation simplex
  * on the cross-scaled integer masses, FP32 Euclidean costs, FP64 objective, one CTA per pair.
  * Same layout as ft_flowtree_estimate_lists (DEVICE docs [nq × docs_ld], out [nq × n_per_q];
- * negative entries score +inf).  Supports are limited to 128 points per side (larger pairs:
+ * negative entries score +inf).  Supports up to m + n ≤ 511 points whose m·n FP32 costs fit one CTA's shared memory (larger pairs:
  * NaN + FT_ERANGE via ft_synchronize); a pivot cap guards against cycling (NaN likewise).     */
 ft_status ft_exact_w1_lists(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
                             const uint32_t* q_w, const int64_t* docs, int64_t docs_ld, int64_t n_per_q, double* out,

@@ -466,12 +466,17 @@ def test_topk_entry_point(ft):
 # ---------------------------------------------------------------------------------------------
 # exact-W1 stage
 # ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("name,nd,nq,per_q", [("reviews", 3000, 6, 12), ("tiny", 100, 4, 10), ("text", 800, 3, 6)])
-def test_exact_w1_matches_lp(ft, name, nd, nq, per_q):
+@pytest.mark.parametrize("start", ["greedy", "nw"])
+@pytest.mark.parametrize("name,nd,nq,per_q", [("reviews", 3000, 6, 12), ("tiny", 100, 4, 10), ("text", 800, 3, 6),
+                                              ("image", 300, 2, 5)])
+def test_exact_w1_matches_lp(ft, name, nd, nq, per_q, start, monkeypatch):
     """Transportation simplex per (query, doc) against the oracle's exact W1 (LP, FP64 costs):
-    within 1e-6 relative (FP32 costs); exact ≤ Flowtree; negative entries score +inf; supports
-    beyond 128 points are NaN (text has docs up to 150)."""
+    within 1e-6 relative (FP32 costs); exact ≤ Flowtree; negative entries score +inf.  Both starting
+    bases (mutual-minimum rounds, plain northwest corner) reach the same optimum; image pairs
+    (170 + 170 points) take the 512-thread variant."""
     import torch
+    if start == "nw":
+        monkeypatch.setenv("FT_EXACT_START", "nw")
     wl = get_workload(name, n_docs=nd, n_queries=nq)
     ix, ds = _setup(ft, wl)
     rng = np.random.default_rng(11)
@@ -481,8 +486,6 @@ def test_exact_w1_matches_lp(ft, name, nd, nq, per_q):
     ex = ft.ft_exact_w1_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, d_docs).cpu().numpy()
     fl = ft.ft_flowtree_estimate_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, d_docs).cpu().numpy()
     assert np.isinf(ex[0, -1]) and np.isinf(fl[0, -1])
-    checked = 0
-    over = False
     for q in range(nq):
         b, bw = wl.query(q)
         for j in range(per_q):
@@ -490,18 +493,40 @@ def test_exact_w1_matches_lp(ft, name, nd, nq, per_q):
             if d < 0:
                 continue
             a, aw = wl.doc(d)
-            if len(a) > 128 or len(b) > 128:
-                assert np.isnan(ex[q, j])
-                over = True
-                continue
             ref = oracle.exact_w1(wl.X, a, aw, b, bw)
             assert abs(ex[q, j] - ref) <= 1e-6 * max(ref, 1e-12), (q, d, ex[q, j], ref)
             assert ex[q, j] <= fl[q, j] * (1 + 1e-6) + 1e-12
-            checked += 1
-    assert checked >= nq * per_q // 3
-    if over:                # the >128-point pairs set the sticky capacity error
-        with pytest.raises(ft.FlowtreeError):
-            ds.synchronize()
+    ds.synchronize()
+
+
+def test_exact_w1_capacity_and_degenerate(ft):
+    """A pair beyond the CTA geometry (300 + 300 points) is NaN with the sticky capacity error;
+    one-point sides reduce to the weighted mean distance (closed form); identical measures give 0."""
+    import torch
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((1000, 4)).astype(np.float32)
+    big = np.sort(rng.choice(1000, 300, replace=False)).astype(np.int32)
+    doc_off = np.array([0, 300, 301, 304], np.int64)
+    ids = np.concatenate([big, [7], [3, 9, 500]]).astype(np.int32)
+    w = np.concatenate([rng.integers(1, 50, 300), [4], [1, 2, 3]]).astype(np.uint32)
+    ix = ft.Index(X, seed=3, max_depth=24)
+    ds = ft.Dataset(ix, doc_off, ids, w)
+    # query 0: 300 points (pairs with doc 0 overflow); query 1: 3 points = doc 2
+    q_off = np.array([0, 300, 303], np.int64)
+    q_ids = np.concatenate([np.sort(rng.choice(1000, 300, replace=False)), [3, 9, 500]]).astype(np.int32)
+    q_w = np.concatenate([rng.integers(1, 50, 300), [1, 2, 3]]).astype(np.uint32)
+    docs = torch.tensor([[0, 1], [1, 2]], dtype=torch.int64).cuda()
+    ex = ft.ft_exact_w1_lists(ds.h, q_off, q_ids, q_w, docs).cpu().numpy()
+    assert np.isnan(ex[0, 0])
+    Xd = X.astype(np.float64)
+    qw = q_w[:300].astype(np.float64)
+    want = float((np.linalg.norm(Xd[q_ids[:300]] - Xd[7], axis=1) * qw).sum() / qw.sum())
+    assert abs(ex[0, 1] - want) <= 1e-6 * want
+    want = float((np.linalg.norm(Xd[[3, 9, 500]] - Xd[7], axis=1) * [1, 2, 3]).sum() / 6)
+    assert abs(ex[1, 0] - want) <= 1e-6 * want
+    assert ex[1, 1] == 0.0
+    with pytest.raises(ft.FlowtreeError):
+        ds.synchronize()
     ds.synchronize()
 
 
