@@ -1,6 +1,6 @@
 """Run single stages of the hot path on the reviews-like config (for ncu captures).
 
-  python tools/kprof.py qt|ft|knn [--queries N]
+  python tools/kprof.py qt|ft|knn|exact [--queries N]
 """
 import argparse
 import os
@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1910_04126_b200 import flowtree as ft, workloads  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("what", choices=["qt", "ft", "knn"])
+p.add_argument("what", choices=["qt", "ft", "knn", "exact"])
 p.add_argument("--queries", type=int, default=1000)
 p.add_argument("--config", default="reviews")
 p.add_argument("--reps", type=int, default=2)
@@ -32,6 +32,9 @@ for _ in range(a.reps):
     elif a.what == "ft":
         out = torch.empty((wl.nq, wl.n), dtype=torch.float64, device=dev)
         ds.flowtree(wl.q_off, qi, qw, out=out, stream=st)
+    elif a.what == "exact":
+        from paper_1910_04126_b200 import pipeline
+        pipeline.knn_qt_ft_exact(ft, ds, wl.q_off, qi, qw, 424, 9, 1, stream=st)
     else:
         oi = torch.empty((wl.nq, wl.k), dtype=torch.int64, device=dev)
         ov = torch.empty((wl.nq, wl.k), dtype=torch.float64, device=dev)

@@ -23,3 +23,13 @@ $F > gpurun_out/kp_ft.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_flowtree" -c 1 -o gpurun_out/prof_ft $F \
   > gpurun_out/ncu_ft.log 2>&1
 echo "ft rc=$?"
+X="python tools/kprof.py ft --queries 64 --reps 1"
+$X > gpurun_out/kp_ftx.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ftx$" -c 1 -o gpurun_out/prof_ftx $X \
+  > gpurun_out/ncu_ftx.log 2>&1
+echo "ftx rc=$?"
+E="python tools/kprof.py exact --queries 1000 --reps 1"
+$E > gpurun_out/kp_exact.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_exact" -c 1 -o gpurun_out/prof_exact $E \
+  > gpurun_out/ncu_exact.log 2>&1
+echo "exact rc=$?"

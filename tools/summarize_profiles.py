@@ -69,7 +69,8 @@ summ = [f"# {rnd}: key metrics from `ncu --set full --clock-control none` (tools
 for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one k_qt launch = 1e8 pairs)"),
                   ("prof_knn.ncu-rep", "kprof knn --queries 200 (first launches of each kernel)"),
                   ("prof_ft.ncu-rep", "kprof ft --queries 16 (exhaustive Flowtree over 100k docs)"),
-                  ("prof_ftx.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree, lane-per-query chunk kernel k_ftx)")]:
+                  ("prof_ftx.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree, lane-per-query chunk kernel k_ftx)"),
+                  ("prof_exact.ncu-rep", "kprof exact --queries 1000 (QT 424 -> FT 9 -> exact W1, transportation simplex)")]:
     p = os.path.join(OUT, rep)
     if not os.path.exists(p):
         continue
