@@ -13,19 +13,21 @@
 //
 // k_dist_tc is persistent (one CTA per SM) and warp specialised over a device-built list of
 // (query, 128-row tile) work items; each query has its own MMA width N = its support rounded up
-// to 16 (≤ 256 per column block), so a batch with a long query does not pad the short ones:
-//   * 8 loader warps, 16 rows each: every lane cp.async-copies 4 16-byte granules of its rows'
-//     32-wide K chunk straight into the A_hi slots of a stage (canonical K-major core-matrix layout,
-//     SWIZZLE_NONE, LBO 128 B, SBO 1024 B), PF chunks ahead of the chunk it converts; once its own
-//     granules have landed (cp.async.wait_group) it splits them in place: hi over the raw value,
-//     lo into the A_lo slot (lane → (row & 7, granule) keeps every 8-lane phase on 8 distinct bank
-//     quads).  No thread waits on a global load: the copy engine carries the latency.  Thread 0
-//     also bulk-copies (cp.async.bulk, mbarrier complete_tx) the query's pre-split B chunk;
-//   * 1 MMA warp: one thread waits the stage's full barrier, issues 4 K-steps × 3 tcgen05.mma
-//     (kind::tf32, M=128, N=N_q) and commits the stage's empty barrier; after the last chunk it
-//     commits the tile's accumulator barrier;
-//   * 4 epilogue warps: tcgen05.ld (32x32b.x16) the accumulator (TMEM double buffer), form the
-//     distance in FP32, force an id present on both sides to exactly 0, write the row.
+// to 16 (≤ 96 per column block), so a batch with a long query does not pad the short ones:
+//   * 4 copy warps cp.async whole 128-byte row segments of the tile's 32-wide K chunk into a
+//     Q-deep raw ring in shared memory (row pitch 144 B), arriving on the slot's mbarrier with
+//     cp.async.mbarrier.arrive.noinc; lane 0 of warp 0 bulk-copies (cp.async.bulk, complete_tx)
+//     the query's pre-split B chunk [B_hi | B_lo] (canonical K-major core-matrix layout,
+//     SWIZZLE_NONE, LBO 128 B, SBO 1024 B);
+//   * 4 converter warps, thread = TMEM lane = tile row: read the raw row, write hi = raw and
+//     lo = x − trunc_tf32(x) into a TMEM A ring with tcgen05.st.32x32b.x32;
+//   * 1 MMA warp: an elected lane waits the slot's full barrier and issues 4 K-steps × 3
+//     tcgen05.mma (kind::tf32, M = 128, N = N_q, A from TMEM): A_hi·B_hi, A_hi·B_lo, A_lo·B_hi into
+//     one accumulator; it commits the slot's empty barrier, and after the last chunk the tile's
+//     accumulator barrier;
+//   * 8 epilogue warps (2 per TMEM lane quarter, alternating 16-column blocks): tcgen05.ld the
+//     double-buffered accumulator, form the distance in FP32 (branch-free MUFU square root), force an
+//     id present on both sides to exactly 0, write the rows coalesced through a per-warp transpose.
 // k_tile_plan / k_tiles build the work list, k_dist_prep the per-query pre-split B chunks.
 //
 // Candidate vocabulary for the prefiltered pipeline: k_vocab marks every vocab id of the query's
@@ -42,7 +44,7 @@ namespace {
 
 constexpr int TM = 128;                 // rows per work item = UMMA M
 constexpr int KC = 32;                  // K elements per chunk (128 B per row)
-constexpr int NCB = 96;                 // query points per column block (accumulator 2 N ≤ 192 columns)
+constexpr int NCB = 96;                 // query points per column block (accumulator N ≤ 96 columns)
 constexpr int SBO = (KC / 4) * 128;     // B operand: bytes between 8-row core-matrix groups
 constexpr int RPITCH = KC * 4 + 16;     // raw ring row pitch (bytes): conflict-free row- and granule-wise access
 constexpr int NCOPY = 128;              // copy threads (warps 0-3)
@@ -56,6 +58,13 @@ constexpr uint32_t TMEM_COLS = 512;     // [0, 2 accw) double-buffered accumulat
 constexpr int TPITCH = 20;              // epilogue transpose buffer pitch (floats): conflict-free float4 rows
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// one elected lane of a converged warp; ptxas then knows the tcgen05.mma operands are uniform
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     // K-major, SWIZZLE_NONE: start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4 [32,46), version 1 [46,48)
@@ -148,7 +157,7 @@ struct DistArgs {
     int cb;                     // column block (query points cb*256 ...)
     int NPmax;                  // B stage capacity: max N_q of the launch
     int Q;                      // raw ring depth (chunks in flight)
-    int accw;                   // accumulator columns per buffer = 2 NPmax ([hi·hi + lo·hi | hi·lo])
+    int accw;                   // accumulator columns per buffer = NPmax
     int naslot;                 // TMEM A ring slots = (512 − 2 accw) / (2 KC)
 };
 
@@ -318,26 +327,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
             const int b = k & 1;
             const int np = a.wdesc[w].w;
             const uint32_t idesc = idesc0 | ((uint32_t)(np >> 3) << 17);
-            const uint32_t idesc2 = idesc0 | ((uint32_t)(np >> 2) << 17);      // N = 2 np: [B_hi | B_lo]
+            const uint32_t blo = (uint32_t)np * KC * 4;                        // B_lo follows B_hi (np rows)
             if (k >= 2) TW(0, mbar_wait(&acce[b], ((k >> 1) - 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t dt = tmem + (uint32_t)(b * a.accw);
             for (int cc = 0; cc < a.nch; cc++) {
                 TW(1, mbar_wait(&full[p], fph));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                if (lane == 0) {
+                if (elect_one()) {
                     const uint32_t ta = tmem + ACC_COLS + (uint32_t)(p * 2 * KC);
                     const uint32_t bs = smem_u32(bring + (size_t)p * b_slot);
 #pragma unroll
                     for (int ks = 0; ks < KC / 8; ks++) {
-                        // D[:, 0:2np) (+)= A_hi·[B_hi | B_lo];  D[:, 0:np) += A_lo·B_hi   (A from TMEM)
+                        // D[:, 0:np) (+)= A_hi·B_hi;  += A_hi·B_lo;  += A_lo·B_hi   (A from TMEM)
                         const uint32_t ah = ta + 8 * ks, al = ta + KC + 8 * ks;
-                        const uint64_t bh = umma_desc(bs + 256 * ks);
+                        const uint64_t bh = umma_desc(bs + 256 * ks), bl = umma_desc(bs + blo + 256 * ks);
                         const uint32_t acc0 = (cc > 0 || ks > 0) ? 1u : 0u;
                         asm volatile(
                             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
-                            "r"(ah), "l"(bh), "r"(idesc2), "r"(acc0));
+                            "r"(ah), "l"(bh), "r"(idesc), "r"(acc0));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(dt), "r"(ah),
+                                     "l"(bl), "r"(idesc));
                         asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(dt), "r"(al),
                                      "l"(bh), "r"(idesc));
                     }
@@ -405,7 +416,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.accw);
             for (int c0 = 16 * half; c0 < np; c0 += 32) {
-                uint32_t v[16], vl[16];
+                uint32_t v[16];
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
                     "%13, %14, %15}, [%16];"
@@ -413,13 +424,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
                       "=r"(v[15])
                     : "r"(tb + (uint32_t)c0));
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-                    "%13, %14, %15}, [%16];"
-                    : "=r"(vl[0]), "=r"(vl[1]), "=r"(vl[2]), "=r"(vl[3]), "=r"(vl[4]), "=r"(vl[5]), "=r"(vl[6]),
-                      "=r"(vl[7]), "=r"(vl[8]), "=r"(vl[9]), "=r"(vl[10]), "=r"(vl[11]), "=r"(vl[12]), "=r"(vl[13]),
-                      "=r"(vl[14]), "=r"(vl[15])
-                    : "r"(tb + (uint32_t)(np + c0)));
                 TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
                 if (c0 >= nb || valid == 0u) continue;
                 const long long tc0 = clock64();
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                     const uint32_t idv[4] = {id4.x, id4.y, id4.z, id4.w};
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        const float dot = __uint_as_float(v[i + u]) + __uint_as_float(vl[i + u]);
+                        const float dot = __uint_as_float(v[i + u]);
                         const float d2 = fmaxf(fmaf(-2.f, dot, nx + nyv[u]), 0.f);
                         float sq;
                         asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(d2));
@@ -728,7 +732,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     const size_t raw_bytes = (size_t)TM * RPITCH;
     const size_t b_slot = 2 * (size_t)a.NPmax * KC * 4;
     const size_t fixed = 2 * NCB * 4 + NEPI * 32 * TPITCH * 4 + 512;
-    a.accw = 2 * a.NPmax;
+    a.accw = a.NPmax;
     a.naslot = std::min(MAXASLOT, (int)(TMEM_COLS - 2 * a.accw) / (2 * KC));
     if (a.naslot < 2) return cudaErrorInvalidConfiguration;
     const size_t budget = 224 * 1024 - fixed - (size_t)MAXASLOT * b_slot;

@@ -8,7 +8,9 @@
 // memory.  Exact for any amount of ties — the Quadtree keys at d = 300 take only a few hundred
 // distinct values over 10^5 docs.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "ft_device.cuh"
 
@@ -33,6 +35,89 @@ __device__ __forceinline__ unsigned digit_of(unsigned long long hi, uint32_t lo,
 // warp-aggregated positions) and bitonic-sort the gathered (key, id) pairs; the first k are the
 // answer.  Exact whenever k ≤ count(≤ t) ≤ capacity; otherwise the row is flagged for the radix
 // kernel.  Two passes over the row instead of up to twelve.
+
+// Block-wide rank selection over keys in shared memory (512 threads): the r-th smallest (0-based)
+// of n composite keys (h, l) — or of h alone when l is null (ties then share the answer's h) — by
+// MSD radix with 8-bit digits, starting at the first byte where the smallest and largest keys
+// differ.  Per pass: a 256-bin histogram of the keys still matching the selected prefix
+// (warp-aggregated with __match_any_sync, so a hot bin takes one atomic per warp), warp 0 finds
+// the bin holding rank r.  Every thread returns the selected (h, l).
+struct SelScratch {
+    unsigned hist[256];
+    unsigned long long ph, mn, mx;
+    uint32_t pl;
+    int need, byte0;
+};
+
+__device__ void block_rank_select(const unsigned long long* h, const uint32_t* l, int n, int r, SelScratch& sc,
+                                  unsigned long long& out_h, uint32_t& out_l) {
+    const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = tid; i < n; i += nt) { mn = min(mn, h[i]); mx = max(mx, h[i]); }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (tid == 0) { sc.mn = ~0ull; sc.mx = 0ull; sc.need = r; sc.pl = 0; }
+    __syncthreads();
+    if (lane == 0) { atomicMin(&sc.mn, mn); atomicMax(&sc.mx, mx); }
+    __syncthreads();
+    const int common = sc.mn == sc.mx ? 64 : __clzll((long long)(sc.mn ^ sc.mx));
+    const int b0 = common / 8;                           // bytes of h shared by every key
+    unsigned long long ph = b0 ? (sc.mn & (~0ull << (64 - 8 * b0))) : 0ull;
+    uint32_t pl = 0;
+    const int nd = l ? 12 : 8;
+    for (int t = b0; t < nd; t++) {
+        for (int b = tid; b < 256; b += nt) sc.hist[b] = 0;
+        __syncthreads();
+        const unsigned long long mh = t == 0 ? 0ull : (t <= 8 ? ~0ull << (64 - 8 * t) : ~0ull);
+        const uint32_t ml = t <= 8 ? 0u : ~0u << (32 - 8 * (t - 8));
+        for (int i0 = 0; i0 < n; i0 += nt) {
+            const int i = i0 + tid;
+            bool in = false;
+            unsigned dg = 0;
+            if (i < n) {
+                const unsigned long long hh = h[i];
+                const uint32_t ll = l ? l[i] : 0u;
+                in = (hh & mh) == ph && (ll & ml) == pl;
+                dg = t < 8 ? (unsigned)((hh >> (56 - 8 * t)) & 255ull) : (unsigned)((ll >> (24 - 8 * (t - 8))) & 255u);
+            }
+            const unsigned act = __ballot_sync(0xffffffffu, in);
+            if (in) {
+                const unsigned grp = __match_any_sync(act, dg);
+                if (lane == __ffs(grp) - 1) atomicAdd(&sc.hist[dg], (unsigned)__popc(grp));
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const unsigned need = (unsigned)sc.need;     // read before the shuffles order the write
+            unsigned c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; j++) { c[j] = sc.hist[8 * lane + j]; sum += c[j]; }
+            unsigned incl = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            unsigned cum = incl - sum;
+            const bool mine = cum <= need && need < incl;
+            if (mine) {
+                int j = 0;
+                while (cum + c[j] <= need) { cum += c[j]; j++; }
+                const unsigned dgt = 8 * lane + j;
+                sc.need = (int)(need - cum);
+                if (t < 8) sc.ph = ph | ((unsigned long long)dgt << (56 - 8 * t));
+                else sc.pl = pl | (dgt << (24 - 8 * (t - 8)));
+            }
+        }
+        __syncthreads();
+        if (t < 8) ph = sc.ph; else pl = sc.pl;
+    }
+    out_h = ph;
+    out_l = pl;
+    __syncthreads();
+}
+
 constexpr int SEL_CAP = 8192;
 constexpr int SEL_SAMPLE = 4096;
 
@@ -54,6 +139,9 @@ __device__ void sort_pairs(unsigned long long* h, uint32_t* l, int P) {
     }
 }
 
+__device__ unsigned long long g_seldbg[8];
+
+template <bool DBG, int GU>
 __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ vals, int64_t vals_ld,
                                                      const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L,
                                                      int k, int64_t* __restrict__ out_ids,
@@ -62,32 +150,42 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;                      // SEL_CAP
     uint32_t* bl = (uint32_t*)(sbuf + SEL_CAP);         // SEL_CAP
-    __shared__ unsigned long long s_thr;
+    __shared__ SelScratch sc;
     __shared__ int s_cnt;
     const int row = blockIdx.x;
     const double* v = vals + (int64_t)row * vals_ld;
     const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
     const int kk = (int)min((int64_t)k, L);
     const int lane = threadIdx.x & 31;
+    long long t0 = DBG ? clock64() : 0, t1 = 0, t2 = 0, t3 = 0;
     if (threadIdx.x == 0) s_cnt = 0;
     unsigned long long thr = ~0ull;
     if (L > SEL_CAP) {
         // strided sample of S keys, sorted; threshold = sample key at the k/L quantile + margin
         const int S = SEL_SAMPLE;
-        for (int j = threadIdx.x; j < S; j += blockDim.x) bh[j] = okey(v[(int64_t)j * L / S]);
-        __syncthreads();
-        fti_bitonic_sort_u64(bh, S);
-        if (threadIdx.x == 0) {
-            const double ex = (double)kk * S / (double)L;
-            const int ti = min(S - 1, (int)(ex + 4.0 * sqrt(ex) + 8.0));
-            s_thr = bh[ti];
+        {
+            constexpr int SU = SEL_SAMPLE / 512;        // all of a thread's sample loads in flight at once
+            double sv[SU];
+#pragma unroll
+            for (int u = 0; u < SU; u++) {
+                const int j = u * 512 + threadIdx.x;
+                sv[u] = j < S ? v[(int64_t)j * L / S] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < SU; u++) {
+                const int j = u * 512 + threadIdx.x;
+                if (j < S) bh[j] = okey(sv[u]);
+            }
         }
         __syncthreads();
-        thr = s_thr;
+        const double ex = (double)kk * S / (double)L;
+        const int ti = min(S - 1, (int)(ex + 4.0 * sqrt(ex) + 8.0));
+        uint32_t dummy;
+        block_rank_select(bh, nullptr, S, ti, sc, thr, dummy);
     }
-    // gather every key ≤ thr (all of them when L ≤ SEL_CAP); 8 loads in flight per thread, then
+    if (DBG) t1 = clock64();
+    // gather every key ≤ thr (all of them when L ≤ SEL_CAP); GU loads in flight per thread, then
     // warp-aggregated positions
-    constexpr int GU = 8;
     for (int64_t i0 = 0; i0 < L; i0 += (int64_t)blockDim.x * GU) {
         double vv[GU];
 #pragma unroll
@@ -112,15 +210,53 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
         }
     }
     __syncthreads();
+    if (DBG) t2 = clock64();
     const int cnt = s_cnt;
     if (cnt < kk || cnt > SEL_CAP) {       // threshold too low or too many ties: radix kernel
         if (threadIdx.x == 0) redo[atomicAdd(nredo, 1)] = row;
         return;
     }
-    const int P = fti_pow2_at_least(max(cnt, 2));
-    for (int i = cnt + threadIdx.x; i < P; i += blockDim.x) { bh[i] = ~0ull; bl[i] = 0xFFFFFFFFu; }
+    int nk = cnt;
+    if (cnt > 2048 && cnt > kk && kk > 0) {    // small sets sort faster than they rank-select
+        // the kk-th smallest gathered (key, id) — composites are distinct — then keep the kk keys
+        // at or below it (positions by warp-aggregated atomics: the sort below fixes the order)
+        unsigned long long th;
+        uint32_t tl;
+        block_rank_select(bh, bl, cnt, kk - 1, sc, th, tl);
+        constexpr int PER = SEL_CAP / 512;
+        unsigned long long kh[PER];
+        uint32_t kl[PER];
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int i = j * blockDim.x + threadIdx.x;
+            kh[j] = i < cnt ? bh[i] : ~0ull;
+            kl[j] = i < cnt ? bl[i] : 0xFFFFFFFFu;
+        }
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const int i = j * blockDim.x + threadIdx.x;
+            const bool keep = i < cnt && (kh[j] < th || (kh[j] == th && kl[j] <= tl));
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (bal == 0u) continue;
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_cnt, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (keep) {
+                const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                bh[pos] = kh[j];
+                bl[pos] = kl[j];
+            }
+        }
+        __syncthreads();
+        nk = kk;
+    }
+    const int P = fti_pow2_at_least(max(nk, 2));
+    for (int i = nk + threadIdx.x; i < P; i += blockDim.x) { bh[i] = ~0ull; bl[i] = 0xFFFFFFFFu; }
     __syncthreads();
     sort_pairs(bh, bl, P);
+    if (DBG) t3 = clock64();
     for (int t = threadIdx.x; t < k; t += blockDim.x) {
         int64_t oid = -1;
         double ov = __longlong_as_double(0x7ff0000000000000ll);
@@ -130,6 +266,14 @@ __global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ 
         }
         out_ids[(int64_t)row * out_ld + t] = oid;
         out_val[(int64_t)row * out_ld + t] = ov;
+    }
+    if (DBG && threadIdx.x == 0) {
+        atomicAdd(&g_seldbg[0], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_seldbg[1], (unsigned long long)(t2 - t1));
+        atomicAdd(&g_seldbg[2], (unsigned long long)(t3 - t2));
+        atomicAdd(&g_seldbg[3], (unsigned long long)(clock64() - t3));
+        atomicAdd(&g_seldbg[4], 1ull);
+        atomicAdd(&g_seldbg[5], (unsigned long long)cnt);
     }
 }
 
@@ -258,10 +402,23 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     e = cudaMemsetAsync(nredo, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     const size_t smem_f = (size_t)SEL_CAP * 12;
-    e = cudaFuncSetAttribute(k_select_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+    const bool dbg = getenv("FT_SELECT_DBG") != nullptr;
+    auto kf = L > SEL_CAP ? (dbg ? k_select_fast<true, 16> : k_select_fast<false, 16>)
+                          : (dbg ? k_select_fast<true, 2> : k_select_fast<false, 2>);
+    e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
     if (e != cudaSuccess) return e;
-    k_select_fast<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo,
-                                             nredo, id_base);
+    kf<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo, nredo,
+                                  id_base);
+    if (dbg) {
+        unsigned long long h[8];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_seldbg, sizeof(h));
+        const double c = h[4] ? (double)h[4] : 1.0;
+        fprintf(stderr, "select dbg per CTA (kcyc): sample %.1f gather %.1f sort %.1f out %.1f | cnt %.0f rows %.0f\n",
+                h[0] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3, h[3] / c / 1e3, h[5] / c, c);
+        memset(h, 0, sizeof(h));
+        cudaMemcpyToSymbol(g_seldbg, h, sizeof(h));
+    }
     // pass 2: MSD radix selection of the listed rows (CTAs past the list exit at once)
     k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P, redo,
                                       nredo, id_base);

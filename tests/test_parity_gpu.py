@@ -463,6 +463,24 @@ def test_topk_entry_point(ft):
         assert np.array_equal(ov2[r].cpu().numpy(), vals[r][o2])
 
 
+@pytest.mark.parametrize("L,k,levels", [(100000, 1500, 400), (100000, 3000, 50), (60000, 1000, 3), (9000, 700, 1000)])
+def test_topk_large_rows_rank_select(ft, L, k, levels):
+    """Rows longer than the 8192-key buffer: sample threshold, gather, then the shared-memory radix
+    rank-select of the k-th (value, id) when more than 2048 keys were gathered (heavy ties: few
+    distinct values), or the radix kernel when the gather overflows; all against numpy."""
+    import torch
+    rng = np.random.default_rng(L + k + levels)
+    vals = rng.integers(0, levels, size=(6, L)).astype(np.float64) * 0.5 + 1.0
+    vals[1] = rng.standard_normal(L)                        # no ties, negative values
+    dv = torch.from_numpy(vals).cuda()
+    oi, ov = ft.ft_topk(dv, k)
+    oi, ov = oi.cpu().numpy(), ov.cpu().numpy()
+    for r in range(6):
+        o = np.lexsort((np.arange(L), vals[r]))[:k]
+        assert np.array_equal(oi[r], o), r
+        assert np.array_equal(ov[r], vals[r][o])
+
+
 # ---------------------------------------------------------------------------------------------
 # exact-W1 stage (SURVEY §8(f) row 1)
 # ---------------------------------------------------------------------------------------------
