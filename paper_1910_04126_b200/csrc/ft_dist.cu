@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
     }
     if (DBG) {
         const unsigned long long tt = (unsigned long long)(clock64() - tstart);
-        if (t == NCOPY) { atomicAdd(&g_dbg[14], dbg[1]); }
+        if (t == NCOPY) { atomicAdd(&g_dbg[14], dbg[1]); atomicAdd(&g_dbg[15], dbg[0]); atomicAdd(&g_dbg[11], tt); }
         if (t == 0) { atomicAdd(&g_dbg[13], (unsigned long long)(w_end - w_begin)); atomicAdd(&g_dbg[0], tt); atomicAdd(&g_dbg[1], dbg[0]); atomicAdd(&g_dbg[2], dbg[1]); atomicAdd(&g_dbg[12], 1ull); }
         if (t == NLOAD) { atomicAdd(&g_dbg[3], tt); atomicAdd(&g_dbg[4], dbg[0]); atomicAdd(&g_dbg[5], dbg[1]); }
         if (t == NLOAD + 32) { atomicAdd(&g_dbg[6], tt); atomicAdd(&g_dbg[7], dbg[0]); atomicAdd(&g_dbg[8], dbg[1]); atomicAdd(&g_dbg[9], dbg[2]); }
@@ -757,8 +757,8 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
             cudaStreamSynchronize(st);
             cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
             const double n = h[12] ? (double)h[12] * 1e3 : 1.0;
-            fprintf(stderr, "dist dbg per CTA (kcyc): copy total %.1f wait_empty %.1f conv wait_raw %.1f | mma total %.1f wait_acce %.1f wait_full %.1f | epi total %.1f wait_accf %.1f tmem_ld %.1f math %.1f | tiles %.1f\n",
-                    h[0] / n, h[1] / n, h[14] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n, h[9] / n, (double)h[13] / (n / 1e3));
+            fprintf(stderr, "dist dbg per CTA (kcyc): copy total %.1f wait_empty %.1f conv total %.1f wait_raw %.1f wait_aslot %.1f | mma total %.1f wait_acce %.1f wait_full %.1f | epi total %.1f wait_accf %.1f tmem_ld %.1f math %.1f | tiles %.1f\n",
+                    h[0] / n, h[1] / n, h[11] / n, h[14] / n, h[15] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n, h[9] / n, (double)h[13] / (n / 1e3));
             memset(h, 0, sizeof(h));
             cudaMemcpyToSymbol(g_dbg, h, sizeof(h));
         }
