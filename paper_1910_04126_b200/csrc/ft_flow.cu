@@ -221,6 +221,52 @@ __device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& c
         int ai = lo, bi = t0 - lo;
         const uint32_t ma = ai ? c.dcum[ai - 1] : 0u, mb = bi ? c.qcum[bi - 1] : 0u;
         uint32_t m = ma > mb ? ma : mb;
+        if (c.trow_base) {
+            // table pricing in batches of RB triples: walk the merge (shared memory only), then issue
+            // every vocab-map load, then every table load, so a batch pays two memory latencies
+            // instead of two per triple; the FP32 accumulation order is the sequential one
+            constexpr int RB = 4;
+            const FtArgs& fa = *c.a;
+            for (int tb = t0; tb < t1; tb += RB) {
+                uint32_t ex[RB], xv[RB];
+                int jv[RB];
+#pragma unroll
+                for (int u = 0; u < RB; u++) {
+                    ex[u] = 0u; xv[u] = 0u; jv[u] = 0;
+                    if (tb + u < t1) {
+                        const uint32_t va = ai < la ? c.dcum[ai] : 0xFFFFFFFFu;
+                        const uint32_t vb = bi < lb ? c.qcum[bi] : 0xFFFFFFFFu;
+                        const bool takeA = va <= vb;
+                        const uint32_t nxt = takeA ? va : vb;
+                        if (nxt > m && ai < la && bi < lb) {
+                            const uint32_t x = c.dvoc[ai] & FTI_VOCAB_MASK;
+                            const uint32_t y = c.qitem[bi].x & FTI_VOCAB_MASK;
+                            if (x != y) { ex[u] = nxt - m; xv[u] = x; jv[u] = bi; }
+                            emit<EXPORT>(fa, x, y, nxt - m, 0u);
+                        }
+                        m = nxt;
+                        if (takeA) ai++; else bi++;
+                    }
+                }
+                uint32_t rv[RB];
+                if (c.map) {
+                    uint2 mw[RB];
+#pragma unroll
+                    for (int u = 0; u < RB; u++) mw[u] = ex[u] ? c.map[xv[u] >> 5] : make_uint2(0u, 0u);
+#pragma unroll
+                    for (int u = 0; u < RB; u++) rv[u] = mw[u].y + __popc(mw[u].x & ((1u << (xv[u] & 31)) - 1u));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < RB; u++) rv[u] = xv[u];
+                }
+                float dv[RB];
+#pragma unroll
+                for (int u = 0; u < RB; u++) dv[u] = ex[u] ? c.trow_base[(int64_t)rv[u] * fa.tab.ld + jv[u]] : 0.f;
+#pragma unroll
+                for (int u = 0; u < RB; u++)
+                    if (ex[u]) acc = fmaf((float)ex[u], dv[u], acc);
+            }
+        } else
         for (int t = t0; t < t1; t++) {
             const uint32_t va = ai < la ? c.dcum[ai] : 0xFFFFFFFFu;
             const uint32_t vb = bi < lb ? c.qcum[bi] : 0xFFFFFFFFu;
