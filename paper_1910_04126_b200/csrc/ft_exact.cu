@@ -102,6 +102,7 @@ struct ExArgs {
     uint32_t* err;
     ExGeom g;
     int greedy;
+    int q0;                     // first query of this launch (grid.y ≤ 65535)
 };
 
 __device__ unsigned long long g_exdbg[10];
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(NT) k_exact(ExArgs a) {
     __shared__ int s_enter, s_done, s_lca, s_x, s_ra, s_ca, s_k;
     __shared__ float s_maxc;
 
-    const int q = blockIdx.y;
+    const int q = a.q0 + (int)blockIdx.y;
     const int64_t slot_j = blockIdx.x;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
@@ -563,7 +564,11 @@ cudaError_t ex_launch(const ExArgs& a, dim3 grid, cudaStream_t st, bool dbg) {
     auto kern = dbg ? k_exact<NT, true> : k_exact<NT, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.g.bytes);
     if (e != cudaSuccess) return e;
-    kern<<<grid, NT, a.g.bytes, st>>>(a);
+    ExArgs b = a;
+    for (unsigned q0 = 0; q0 < grid.y; q0 += 65535) {
+        b.q0 = (int)q0;
+        kern<<<dim3(grid.x, std::min(65535u, grid.y - q0)), NT, a.g.bytes, st>>>(b);
+    }
     return cudaSuccess;
 }
 

@@ -59,6 +59,7 @@ struct FtArgs {
     const uint32_t* fb_list;     // list mode: [nq][fb_cap] doc positions handed over by k_ftx
     const uint32_t* fb_cnt;      // [nq]
     int64_t fb_cap;
+    int32_t q0;                  // first query of this launch (grid.y ≤ 65535)
 };
 
 constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
@@ -289,7 +290,7 @@ __device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& c
 template <bool EXPORT>
 __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    const int q = blockIdx.y;
+    const int q = a.q0 + (int)blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
     const QHeader* hdr = (const QHeader*)slot;
     // shared layout: qitem[Sq] uint2 | vocab lookup: bitmap[nw] + rank[nw] u32, or hash[vh_cap] uint2 |
@@ -506,15 +507,13 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
             return e;
         }
     }
-    if (d_flow) {
-        e = cudaFuncSetAttribute(k_flowtree<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_flowtree<true><<<dim3((unsigned)bx, (unsigned)nq), FT_WARPS * 32, smem, st>>>(a);
-    } else {
-        e = cudaFuncSetAttribute(k_flowtree<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_flowtree<false><<<dim3((unsigned)bx, (unsigned)nq), FT_WARPS * 32, smem, st>>>(a);
+    auto kern = d_flow ? k_flowtree<true> : k_flowtree<false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    for (int32_t q0 = 0; q0 < nq; q0 += 65535) {          // grid.y ≤ 65535 queries per launch
+        a.q0 = q0;
+        kern<<<dim3((unsigned)bx, (unsigned)std::min(65535, nq - q0)), FT_WARPS * 32, smem, st>>>(a);
+        fti_count_launches(1);
     }
-    fti_count_launches(1);
     return cudaGetLastError();
 }

@@ -568,3 +568,28 @@ def test_three_stage_pipeline_matches_oracle(ft):
         if ids[q, 0] != surv[best]:
             got = list(surv).index(ids[q, 0])
             assert abs(ex[got] - ex[best]) <= 2e-6 * ex[best]
+
+
+def test_more_than_65535_queries(ft):
+    """Query batches beyond one launch's grid.y (65,535) run in slices: the Flowtree and exact-W1
+    values of queries on both sides of the boundary equal the oracle's."""
+    import torch
+    wl = get_workload("tiny")
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    rng = np.random.default_rng(21)
+    nq = 70000
+    q_ids = np.sort(np.stack([rng.choice(wl.X.shape[0], 3, replace=False) for _ in range(nq)]), 1).astype(np.int32)
+    q_w = rng.integers(1, 9, size=(nq, 3)).astype(np.uint32)
+    q_off = np.arange(nq + 1, dtype=np.int64) * 3
+    docs = np.array([0, 7, 42], np.int64)
+    fl = ds.flowtree(q_off, q_ids.ravel(), q_w.ravel(), docs=docs)
+    dl = torch.from_numpy(np.tile(docs, (nq, 1))).cuda()
+    ex = ft.ft_exact_w1_lists(ds.h, q_off, q_ids.ravel(), q_w.ravel(), dl).cpu().numpy()
+    for q in (0, 65534, 65535, 65536, nq - 1):
+        for j, d in enumerate(docs):
+            a, aw = wl.doc(int(d))
+            ref = T.ft(a, aw, q_ids[q], q_w[q])
+            assert abs(fl[q, j] - ref) <= FT_TOL * ref, (q, d)
+            w1 = oracle.exact_w1(wl.X, a, aw, q_ids[q], q_w[q])
+            assert abs(ex[q, j] - w1) <= 1e-6 * w1, (q, d)
