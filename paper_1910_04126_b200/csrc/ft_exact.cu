@@ -428,18 +428,17 @@ __global__ void __launch_bounds__(NT) k_exact(ExArgs a) {
         if (t < V) { pot[t] = pacc[cur * Vx + t]; dep[t] = pdep[cur * Vx + t]; }
         __syncthreads();
         EXT(1);
-        // ---- 2. most negative reduced cost ----
-        int enter = -1;
+        // ---- 2. most negative reduced cost: thread (column j, first row r0), rows r0, r0 + R, … ----
         {
             double bestr = 0.0;
             int bidx = -1;
-            const int di = NT / n, dj = NT - di * n;
-            int i = t / n, j = t - (t / n) * n;
-            for (int c = t; c < m * n; c += NT) {
-                const double r = (double)cost[c] - pot[i] - pot[m + j];
-                if (r < bestr) { bestr = r; bidx = c; }
-                i += di; j += dj;
-                if (j >= n) { j -= n; i++; }
+            const int R = NT / n, j = t % n, r0 = t / n;
+            if (r0 < R) {
+                const double vj = pot[m + j];
+                for (int i = r0; i < m; i += R) {
+                    const double r = (double)cost[i * n + j] - pot[i] - vj;
+                    if (r < bestr) { bestr = r; bidx = i * n + j; }
+                }
             }
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, bestr, o);
@@ -447,34 +446,36 @@ __global__ void __launch_bounds__(NT) k_exact(ExArgs a) {
                 if (ob < bestr || (ob == bestr && oi >= 0 && (bidx < 0 || oi < bidx))) { bestr = ob; bidx = oi; }
             }
             if (lane == 0) { red_v[warp] = bestr; red_i[warp] = bidx; }
-            __syncthreads();
-            double bv = 0.0;
-            int bx = -1;
-            for (int w = 0; w < NW; w++)
-                if (red_v[w] < bv || (red_v[w] == bv && red_i[w] >= 0 && (bx < 0 || red_i[w] < bx))) {
-                    bv = red_v[w];
-                    bx = red_i[w];
-                }
-            enter = (bv < -tol) ? bx : -1;
         }
-        if (t == 0) {
-            s_enter = enter;
-            if (enter < 0) s_done = 1;
-            else if (++piv > max_pivots) s_done = 2;
-            if (s_enter >= 0) {
-                // LCA of row p and column m + qq by binary lifting
-                int x = s_enter / n, y = m + (s_enter - (s_enter / n) * n);
-                if (dep[x] < dep[y]) { const int tt = x; x = y; y = tt; }
-                int diff = dep[x] - dep[y];
-                for (int k = 0; diff; k++, diff >>= 1)
-                    if (diff & 1) x = anc[k * Vx + x];
-                if (x != y) {
-                    for (int k = LOG; k >= 0; k--)
-                        if (anc[k * Vx + x] != anc[k * Vx + y]) { x = anc[k * Vx + x]; y = anc[k * Vx + y]; }
-                    x = anc[x];
+        __syncthreads();
+        if (warp == 0) {                                   // across warps: warp 0, then lane 0 pivots
+            double bv = lane < NW ? red_v[lane] : 0.0;
+            int bx = lane < NW ? red_i[lane] : -1;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bx, o);
+                if (ob < bv || (ob == bv && oi >= 0 && (bx < 0 || oi < bx))) { bv = ob; bx = oi; }
+            }
+            const int enter = (bv < -tol) ? bx : -1;
+            if (lane == 0) {
+                s_enter = enter;
+                if (enter < 0) s_done = 1;
+                else if (++piv > max_pivots) s_done = 2;
+                if (enter >= 0) {
+                    // LCA of row p and column m + qq by binary lifting
+                    int x = enter / n, y = m + (enter - (enter / n) * n);
+                    if (dep[x] < dep[y]) { const int tt = x; x = y; y = tt; }
+                    int diff = dep[x] - dep[y];
+                    for (int k = 0; diff; k++, diff >>= 1)
+                        if (diff & 1) x = anc[k * Vx + x];
+                    if (x != y) {
+                        for (int k = LOG; k >= 0; k--)
+                            if (anc[k * Vx + x] != anc[k * Vx + y]) { x = anc[k * Vx + x]; y = anc[k * Vx + y]; }
+                        x = anc[x];
+                    }
+                    s_lca = x;
+                    s_key = ~0ull;
                 }
-                s_lca = x;
-                s_key = ~0ull;
             }
         }
         __syncthreads();
