@@ -593,3 +593,14 @@ def test_more_than_65535_queries(ft):
             assert abs(fl[q, j] - ref) <= FT_TOL * ref, (q, d)
             w1 = oracle.exact_w1(wl.X, a, aw, q_ids[q], q_w[q])
             assert abs(ex[q, j] - w1) <= 1e-6 * w1, (q, d)
+
+
+def test_knn_table_chunking_invariant(ft, monkeypatch):
+    """The distance tables are built per query chunk (the chunk size follows the free HBM); any
+    chunking gives bit-identical k-NN ids and values (FT_TABLE_CHUNK forces ragged chunks of 3)."""
+    wl = get_workload("reviews", n_docs=3000, n_queries=11)
+    ix, ds = _setup(ft, wl)
+    ids0, v0 = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 300)
+    monkeypatch.setenv("FT_TABLE_CHUNK", "3")
+    ids1, v1 = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 300)
+    assert np.array_equal(ids0, ids1) and np.array_equal(v0, v1)
