@@ -67,7 +67,7 @@ print("\n".join(lines[:16]))
 traffic = {}
 summ = [f"# {rnd}: key metrics from `ncu --set full --clock-control none` (tools/profile_round.sh)", ""]
 for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one k_qt launch = 1e8 pairs)"),
-                  ("prof_knn.ncu-rep", "kprof knn --queries 200 (first launches of each kernel)"),
+                  ("prof_knn.ncu-rep", "kprof knn --queries 1000 (the bench batch: one launch of each kernel per step)"),
                   ("prof_ft.ncu-rep", "kprof ft --queries 16 (exhaustive Flowtree over 100k docs)"),
                   ("prof_ftx.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree, lane-per-query chunk kernel k_ftx)"),
                   ("prof_exact.ncu-rep", "kprof exact --queries 1000 (QT 424 -> FT 9 -> exact W1, transportation simplex)")]:
@@ -92,7 +92,7 @@ for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one
 open(os.path.join(PROF, f"{rnd}_ncu_summary.txt"), "w").write("\n".join(summ) + "\n")
 if traffic:
     traffic["source"] = (f"profiles/{rnd}_ncu_summary.txt: dram read+write of one ncu --set full launch (k_qt: the "
-                         "1000-query bench batch; k_dist_tc / k_flowtree: the first query chunk of kprof knn, the "
-                         "same chunk size the bench uses)")
+                         "1000-query bench batch; k_dist_tc / k_flowtree: kprof knn on the same 1000-query batch, "
+                         "one launch each, as in the bench)")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     print(traffic)
