@@ -20,6 +20,7 @@
 // posting and accumulates ω·min(U m_μ, W m_ν) in a u64 register — no atomics, no per-query
 // probing.  Lane q then finalises the value of (q, doc).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "ft_device.cuh"
@@ -278,6 +279,8 @@ struct QtArgs {
     double* out;
     int64_t out_ld;
     int d_star, l_root;
+    double pow2;                // 2^{ℓ_root − D*} when it is a normal double (0: use scalbn)
+    int wide;                   // D* > 31: the U·A and W·B products can overflow 64 bits
     uint32_t* err;
 };
 
@@ -291,10 +294,11 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
     const unsigned long long Uq = sh.U[lane], Bq = sh.B[lane], W = W32;
     double val;
     bool bad = !sh.ok[lane];
-    bad |= __umul64hi(Uq, A) != 0ull || __umul64hi(W, Bq) != 0ull;
     const unsigned long long ua = Uq * A, wb = W * Bq;
     const unsigned long long tot = ua + wb;
-    bad |= tot < ua;
+    // A, B < 2^16·2^{D*} (masses ≤ 65535 per level): with D* ≤ 31 neither product nor the sum
+    // can overflow
+    if (a.wide) bad |= __umul64hi(Uq, A) != 0ull || __umul64hi(W, Bq) != 0ull || tot < ua;
     const unsigned long long num = tot - (acc << 1);
     if (!bad && num >= (1ull << 53)) {
         bad = true;
@@ -303,7 +307,8 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
     if (bad) {
         val = __longlong_as_double(0x7ff8000000000000ll);
     } else {
-        const double scaled = scalbn((double)num, a.l_root - a.d_star);
+        // exact: num < 2^53 and a power-of-two factor
+        const double scaled = a.pow2 != 0.0 ? (double)num * a.pow2 : scalbn((double)num, a.l_root - a.d_star);
         val = __ddiv_rn(scaled, (double)(Uq * W));
     }
     a.out[(int64_t)q * a.out_ld + dp] = val;
@@ -338,7 +343,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
             const uint32_t um = U32 * (y & 0xFFFFu);
             const uint32_t wm = W32 * mnu;
-            acc += (unsigned long long)(um < wm ? um : wm) << (a.d_star - (int)(y >> 16));
+            acc += (unsigned long long)(um < wm ? um : wm) << (y >> 16);
         };
         for (uint32_t rb = r0; rb < r1; rb += 32) {
             const uint32_t r = rb + lane;
@@ -354,7 +359,8 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             // broadcast loads (every lane reads the same {union id, mass | depth << 16})
             const unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
             const int nh = __popc(hm);
-            if (id >= 0) hq[__popc(hm & lt)] = make_uint2((uint32_t)id, y);
+            // the queue entry carries the shift D* − depth in place of the depth
+            if (id >= 0) hq[__popc(hm & lt)] = make_uint2((uint32_t)id, (y & 0xFFFFu) | ((uint32_t)(a.d_star - (int)(y >> 16)) << 16));
             if (nh & 1) {
                 if (lane == 0) hq[nh] = make_uint2(0u, 0u);      // pad: mass 0 contributes 0
             }
@@ -528,6 +534,8 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
+    a.pow2 = std::abs(a.l_root - a.d_star) <= 960 ? std::ldexp(1.0, a.l_root - a.d_star) : 0.0;
+    a.wide = a.d_star > 31 ? 1 : 0;
     a.err = ds->err_dev;
     const size_t smem = std::max<size_t>(4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap,
                                          dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 8 +
