@@ -321,7 +321,7 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
 // test, no posting search.  The node's depth rides in the doc record (mass | depth << 16).
 __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* __restrict__ bits,
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
-                                              uint2* __restrict__ hq, const ChunkHdr& sh, int nqc) {
+                                              uint4* __restrict__ hq, const ChunkHdr& sh, int nqc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
@@ -339,11 +339,11 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
         const uint32_t W32 = a.W[doc];
         const unsigned long long A = a.A[doc];
         unsigned long long acc = 0;
-        auto term = [&](uint32_t mnu, uint32_t y) {
+        auto term = [&](uint32_t mnu, uint32_t mmu, uint32_t sh_) {
             // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
-            const uint32_t um = U32 * (y & 0xFFFFu);
+            const uint32_t um = U32 * mmu;
             const uint32_t wm = W32 * mnu;
-            acc += (unsigned long long)(um < wm ? um : wm) << (y >> 16);
+            acc += (unsigned long long)(um < wm ? um : wm) << sh_;
         };
         for (uint32_t rb = r0; rb < r1; rb += 32) {
             const uint32_t r = rb + lane;
@@ -356,21 +356,22 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
                 if ((bw >> bpos) & 1u) id = (int)(rank[rec.x >> 5] + __popc(bw & ((1u << bpos) - 1u)));
             }
             // compact the batch's hits into the warp's queue, then visit them two at a time with
-            // broadcast loads (every lane reads the same {union id, mass | depth << 16})
+            // broadcast loads (every lane reads the same {posting offset, m_μ, D* − depth})
             const unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
             const int nh = __popc(hm);
-            // the queue entry carries the shift D* − depth in place of the depth
-            if (id >= 0) hq[__popc(hm & lt)] = make_uint2((uint32_t)id, (y & 0xFFFFu) | ((uint32_t)(a.d_star - (int)(y >> 16)) << 16));
+            // the compacting lane decodes the record once: every lane then reads a ready entry
+            if (id >= 0)
+                hq[__popc(hm & lt)] = make_uint4((uint32_t)id * QT_QC, y & 0xFFFFu, (uint32_t)(a.d_star - (int)(y >> 16)), 0u);
             if (nh & 1) {
-                if (lane == 0) hq[nh] = make_uint2(0u, 0u);      // pad: mass 0 contributes 0
+                if (lane == 0) hq[nh] = make_uint4(0u, 0u, 0u, 0u);      // pad: mass 0 contributes 0
             }
             __syncwarp();
             for (int h = 0; h < nh; h += 2) {
-                const uint2 e1 = hq[h], e2 = hq[h + 1];
-                const uint32_t p1 = post[e1.x * QT_QC + lane];
-                const uint32_t p2 = post[e2.x * QT_QC + lane];
-                term(p1, e1.y);
-                term(p2, e2.y);
+                const uint4 e1 = hq[h], e2 = hq[h + 1];
+                const uint32_t p1 = post[e1.x + lane];
+                const uint32_t p2 = post[e2.x + lane];
+                term(p1, e1.y, e1.z);
+                term(p2, e2.y, e2.z);
             }
             __syncwarp();
         }
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
         const uint32_t* gb = (const uint32_t*)(dsrc + sizeof(DenseHdr));
         const int nwords = 2 * a.dg.mw + (int)dh.nU * QT_QC / 2;    // bits | rank | post, contiguous
         for (int i = threadIdx.x; i < nwords; i += blockDim.x) sm[i] = gb[i];
-        uint2* hq = (uint2*)(sm + ((2 * a.dg.mw + a.dg.cap * QT_QC / 2 + 1) & ~1));   // per-warp hit queues
+        uint4* hq = (uint4*)(sm + ((2 * a.dg.mw + a.dg.cap * QT_QC / 2 + 3) & ~3));   // per-warp hit queues
         __syncthreads();
         qt_scan_dense(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
         return;
@@ -538,8 +539,8 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     a.wide = a.d_star > 31 ? 1 : 0;
     a.err = ds->err_dev;
     const size_t smem = std::max<size_t>(4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap,
-                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 8 +
-                                                          (size_t)QT_WARPS * 32 * 8
+                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 16 +
+                                                          (size_t)QT_WARPS * 32 * 16
                                                     : 0);
     e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
