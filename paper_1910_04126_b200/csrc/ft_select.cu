@@ -142,7 +142,7 @@ __device__ void sort_pairs(unsigned long long* h, uint32_t* l, int P) {
 __device__ unsigned long long g_seldbg[8];
 
 template <bool DBG, int GU>
-__global__ void __launch_bounds__(512) k_select_fast(const double* __restrict__ vals, int64_t vals_ld,
+__global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict__ vals, int64_t vals_ld,
                                                      const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L,
                                                      int k, int64_t* __restrict__ out_ids,
                                                      double* __restrict__ out_val, int64_t out_ld,
@@ -406,6 +406,9 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     auto kf = L > SEL_CAP ? (dbg ? k_select_fast<true, 16> : k_select_fast<false, 16>)
                           : (dbg ? k_select_fast<true, 2> : k_select_fast<false, 2>);
     e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+    if (e != cudaSuccess) return e;
+    // two 98 KB CTAs per SM need the maximum shared-memory carveout
+    e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     kf<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo, nredo,
                                   id_base);
