@@ -119,7 +119,7 @@ __device__ void block_rank_select(const unsigned long long* h, const uint32_t* l
 }
 
 constexpr int SEL_CAP = 8192;
-constexpr int SEL_SAMPLE = 4096;
+constexpr int SEL_SAMPLE = 8192;          // = SEL_CAP: the sample fills the key buffer; ±1/√(rank) count noise
 
 __device__ void sort_pairs(unsigned long long* h, uint32_t* l, int P) {
     for (int kb = 2; kb <= P; kb <<= 1) {
@@ -151,14 +151,15 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
     unsigned long long* bh = sbuf;                      // SEL_CAP
     uint32_t* bl = (uint32_t*)(sbuf + SEL_CAP);         // SEL_CAP
     __shared__ SelScratch sc;
-    __shared__ int s_cnt;
+    __shared__ int s_cnt, s_lt;
+    __shared__ int s_wsum[16];
     const int row = blockIdx.x;
     const double* v = vals + (int64_t)row * vals_ld;
     const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
     const int kk = (int)min((int64_t)k, L);
     const int lane = threadIdx.x & 31;
     long long t0 = DBG ? clock64() : 0, t1 = 0, t2 = 0, t3 = 0;
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) { s_cnt = 0; s_lt = 0; }
     unsigned long long thr = ~0ull;
     if (L > SEL_CAP) {
         // strided sample of S keys, sorted; threshold = sample key at the k/L quantile + margin
@@ -200,8 +201,12 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
             const bool sel = i < L && hi <= thr;
             const unsigned bal = __ballot_sync(0xffffffffu, sel);
             if (bal == 0u) continue;
+            const unsigned blt = __ballot_sync(0xffffffffu, sel && hi < thr);
             int base = 0;
-            if (lane == 0) base = atomicAdd(&s_cnt, __popc(bal));
+            if (lane == 0) {
+                base = atomicAdd(&s_cnt, __popc(bal));
+                if (blt) atomicAdd(&s_lt, __popc(blt));
+            }
             base = __shfl_sync(0xffffffffu, base, 0);
             if (sel) {
                 const int pos = base + __popc(bal & ((1u << lane) - 1u));
@@ -211,12 +216,88 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
     }
     __syncthreads();
     if (DBG) t2 = clock64();
-    const int cnt = s_cnt;
-    if (cnt < kk || cnt > SEL_CAP) {       // threshold too low or too many ties: radix kernel
+    int cnt = s_cnt;
+    const int c_lt = s_lt;
+    int nk = cnt;
+    const bool below_only = cnt > SEL_CAP && c_lt >= kk && c_lt <= SEL_CAP;   // the keys < t suffice
+    const bool tie_fill = cnt > SEL_CAP && !id && c_lt < kk;                   // plus the first ties
+    if (tie_fill || below_only) {
+        // too many keys tie with the threshold for the buffer (the Quadtree values of a large
+        // collection take few distinct values): gather the keys strictly below it, then either
+        // they already hold the answer (rank-select below), or the answer is all of them plus the
+        // first kk − c_lt tied keys in row order (implicit ids = positions: row order is id order)
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        for (int64_t i0 = 0; i0 < L; i0 += (int64_t)blockDim.x * GU) {
+            double vv[GU];
+#pragma unroll
+            for (int u = 0; u < GU; u++) {
+                const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+                vv[u] = i < L ? v[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < GU; u++) {
+                const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+                const unsigned long long hi = okey(vv[u]);
+                const bool sel = i < L && hi < thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, sel);
+                if (bal == 0u) continue;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&s_cnt, __popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (sel) {
+                    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                    bh[pos] = hi;
+                    bl[pos] = id ? (uint32_t)id[i] : (uint32_t)(id_base + i);
+                }
+            }
+        }
+        __syncthreads();
+        cnt = c_lt;
+        nk = c_lt;
+    }
+    if (tie_fill) {
+        const int R = kk - c_lt;
+        // the tied keys in row order: each thread a contiguous run of GU, block prefix of counts
+        const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        int found = 0;
+        for (int64_t i0 = 0; i0 < L && found < R; i0 += (int64_t)blockDim.x * GU) {
+            const int64_t ib = i0 + (int64_t)threadIdx.x * GU;
+            unsigned eqm = 0;
+#pragma unroll
+            for (int u = 0; u < GU; u++)
+                if (ib + u < L && okey(v[ib + u]) == thr) eqm |= 1u << u;
+            const int mine = __popc(eqm);
+            int incl = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            __syncthreads();                         // s_wsum reuse
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            int woff = 0, tot = 0;
+            for (int w = 0; w < nw; w++) {
+                const int x = s_wsum[w];
+                if (w < warp) woff += x;
+                tot += x;
+            }
+            int pos = found + woff + incl - mine;
+            for (int u = 0; u < GU && eqm; u++) {
+                if ((eqm >> u) & 1u) {
+                    if (pos < R) { bh[c_lt + pos] = thr; bl[c_lt + pos] = (uint32_t)(id_base + ib + u); }
+                    pos++;
+                }
+            }
+            found += tot;                            // uniform: every thread summed the same totals
+        }
+        __syncthreads();
+        cnt = kk;
+        nk = kk;
+    } else if (!below_only && (cnt < kk || cnt > SEL_CAP)) {   // threshold too low / ties with ids: radix
         if (threadIdx.x == 0) redo[atomicAdd(nredo, 1)] = row;
         return;
     }
-    int nk = cnt;
     if (cnt > 2048 && cnt > kk && kk > 0) {    // small sets sort faster than they rank-select
         // the kk-th smallest gathered (key, id) — composites are distinct — then keep the kk keys
         // at or below it (positions by warp-aggregated atomics: the sort below fixes the order)

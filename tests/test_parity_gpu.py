@@ -463,11 +463,13 @@ def test_topk_entry_point(ft):
         assert np.array_equal(ov2[r].cpu().numpy(), vals[r][o2])
 
 
-@pytest.mark.parametrize("L,k,levels", [(100000, 1500, 400), (100000, 3000, 50), (60000, 1000, 3), (9000, 700, 1000)])
+@pytest.mark.parametrize("L,k,levels", [(100000, 1500, 400), (100000, 3000, 50), (60000, 1000, 3), (9000, 700, 1000),
+                                         (1000000, 2000, 300), (1000000, 2000, 40000)])
 def test_topk_large_rows_rank_select(ft, L, k, levels):
     """Rows longer than the 8192-key buffer: sample threshold, gather, then the shared-memory radix
-    rank-select of the k-th (value, id) when more than 2048 keys were gathered (heavy ties: few
-    distinct values), or the radix kernel when the gather overflows; all against numpy."""
+    rank-select of the k-th (value, id) when more than 2048 keys were gathered, or — when ties at
+    the threshold overflow the buffer (few distinct values, as the Quadtree keys of a large
+    collection) — every key below it plus the first tied keys in row order; all against numpy."""
     import torch
     rng = np.random.default_rng(L + k + levels)
     vals = rng.integers(0, levels, size=(6, L)).astype(np.float64) * 0.5 + 1.0
@@ -604,3 +606,27 @@ def test_knn_table_chunking_invariant(ft, monkeypatch):
     monkeypatch.setenv("FT_TABLE_CHUNK", "3")
     ids1, v1 = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 300)
     assert np.array_equal(ids0, ids1) and np.array_equal(v0, v1)
+
+
+def test_topk_threshold_tie_blocks(ft):
+    """The two tie-overflow paths of the sample-threshold selection, forced by construction
+    (1M keys, k = 2000, sample threshold inside a tie block larger than the 8192-key buffer):
+    block below the threshold already ≥ k (gather the keys strictly below it), and block below < k
+    (all of them plus the first tied keys in row order)."""
+    import torch
+    rng = np.random.default_rng(77)
+    L, k = 1000000, 2000
+    rows = []
+    for below, tie in ((3000, 6000), (500, 9500), (0, 12000)):
+        v = 3.0 + rng.random(L)
+        pos = rng.permutation(L)
+        v[pos[:below]] = 1.0
+        v[pos[below:below + tie]] = 2.0
+        rows.append(v)
+    vals = np.stack(rows)
+    oi, ov = ft.ft_topk(torch.from_numpy(vals).cuda(), k)
+    oi, ov = oi.cpu().numpy(), ov.cpu().numpy()
+    for r in range(len(rows)):
+        o = np.lexsort((np.arange(L), vals[r]))[:k]
+        assert np.array_equal(oi[r], o), r
+        assert np.array_equal(ov[r], vals[r][o])
