@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
     if (threadIdx.x == 0) { s_cnt = 0; s_lt = 0; }
     unsigned long long thr = ~0ull;
     if (L > SEL_CAP) {
-        // strided sample of S keys, sorted; threshold = sample key at the k/L quantile + margin
-        const int S = SEL_SAMPLE;
+        // strided sample of S keys; threshold = the sample key at the k/L quantile + margin.  The
+        // full 8192-key sample only when the quantile rank of a half sample would be small (the
+        // count noise is ±1/√rank)
+        const int S = (int64_t)kk * (SEL_SAMPLE / 2) < 32 * L ? SEL_SAMPLE : SEL_SAMPLE / 2;
         {
             constexpr int SU = SEL_SAMPLE / 512;        // all of a thread's sample loads in flight at once
             double sv[SU];
