@@ -491,13 +491,17 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     const size_t ysm = a.small_d ? (size_t)a.Sq * a.d * 4 : 0;
     size_t smem = (size_t)a.Sq * 8 + lookup + ysm + (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
     cudaError_t e;
-    // exhaustive scoring with a distance table and a star-like tree: the lane-per-query chunk kernel
-    // (ft_flowx.cu) scores every pair it can and lists the rest for this kernel (list mode)
-    if (!d_flow && !d_docs && tab.table && !tab.map && a.use_bitmap && ds->n_mn <= 2 * ds->n &&
-        L.smax <= FTX_MAX_SQ && !getenv("FT_GENERAL_ONLY")) {
+    // with a distance table and a star-like tree, the lane-per-pair kernel (ft_flowd.cu; or, for
+    // exhaustive scoring with FT_FTX=1, the lane-per-query chunk kernel ft_flowx.cu) scores every
+    // pair it can and lists the rest for this kernel (list mode)
+    if (!d_flow && tab.table && a.use_bitmap && ds->n_mn <= 2 * ds->n && L.smax <= FTX_MAX_SQ &&
+        !getenv("FT_GENERAL_ONLY")) {
         uint32_t* fl = nullptr;
         uint32_t* fc = nullptr;
-        e = fti_launch_ftx(ds, L, d_qblock, nq, n_docs, tab, d_out, out_ld, &fl, &fc, st);
+        if (!d_docs && !tab.map && getenv("FT_FTX"))
+            e = fti_launch_ftx(ds, L, d_qblock, nq, n_docs, tab, d_out, out_ld, &fl, &fc, st);
+        else
+            e = fti_launch_ftd(ds, L, d_qblock, nq, d_docs, docs_ld, n_docs, tab, d_out, out_ld, &fl, &fc, st);
         if (e == cudaSuccess) {
             a.fb_list = fl;
             a.fb_cnt = fc;

@@ -1,0 +1,337 @@
+// ft_flowd.cu — a6 with LANE = PAIR: the Flowtree estimate (§3; greedy flow
+// PAPER.md:495-504) of 32 (query, doc) pairs per warp that share the query.
+//
+// A CTA works for one query: its items, its vocab bitmap + per-word rank (query item index of an
+// id) and, for a compact candidate table, its row map ({bits, rank} per 32 vocab ids) sit in
+// shared memory.  Lane l of a warp scores the pair (q, docs[base + l]) on its own:
+//   * M-nodes: a cell with ≥ 2 ground points present on both sides (phase B of the warp kernel)
+//     hands the pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
+//   * self matches (reading R8): one pass over the doc items tests the query bitmap and queues
+//     the shared ids {doc index i, query index j, w} in increasing vocab order, so both sides of
+//     the merge below consume the queue with a monotone cursor;
+//   * root: the northwest corner over the residuals in vocab order (reading R10) as a sequential
+//     two-pointer — η = min of the current residuals, the exhausted side advances — with the next
+//     next doc items in a register pipeline (raw records loaded two advances ahead).  The merge
+//     advances in warp-uniform batches of
+//     DRB steps; every lane then issues its DRB table gathers together.
+// All pairs of a CTA read one query's table, so the gathers of a warp hit one L2-resident table
+// (the warp kernel and the lane-per-query kernel spread them over many tables).  Masses are exact
+// u32 (reading R13), distances FP32 from the a5 table, sums FP32 per batch and FP64 across
+// batches — the same triples and the same arithmetic as k_flowtree's root merge.
+#include <algorithm>
+
+#include "ft_device.cuh"
+
+namespace {
+
+constexpr int DW = 8;      // warps per CTA
+constexpr int DCAP = 32;   // shared ids per pair held in the per-lane queue
+constexpr int DRB = 8;     // merge steps per gather batch
+constexpr uint32_t DQ_END = 0xFFFFFFFFu;   // queue sentinel: i = j = 255 never matches (s, sq ≤ 255)
+
+struct DArgs {
+    const uint32_t* doc_off;
+    const uint2* items;
+    const uint32_t* Wd;
+    const uint32_t* mn_off;
+    const uint4* mnodes;
+    const uint8_t* qblock;
+    QueryLayout L;
+    int32_t q0;
+    const int64_t* docs;       // [nq][docs_ld] candidate docs, or null (position = doc)
+    int64_t docs_ld, n_docs, n;
+    const float* table;
+    const uint2* map;          // [nq][nw] {bits, rank} rows of the compact table, or null (row = vocab id)
+    const int64_t* row_base;   // [nq] or null (q * rows_cap)
+    int64_t rows_cap;
+    int32_t ld;
+    int32_t nw, Sq;
+    double* out;
+    int64_t out_ld;
+    uint32_t* fb_list;
+    uint32_t* fb_cnt;
+    int64_t fb_cap;
+    uint32_t* err;
+    unsigned long long* units;
+};
+
+__global__ void __launch_bounds__(DW * 32, 2) k_ftd(DArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int q = a.q0 + (int)blockIdx.y;
+    const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
+    const QHeader* hdr = (const QHeader*)slot;
+    // shared: qitem[Sq] uint2 | smap[nw] uint2 (compact table) | qbits[nw] | qrank[nw] | queue[DW][DCAP][32]
+    uint2* qitem = (uint2*)sm;
+    uint2* smap = qitem + a.Sq;
+    uint32_t* qbits = (uint32_t*)(smap + (a.map ? a.nw : 0));
+    uint32_t* qrank = qbits + a.nw;
+    uint32_t* queue = qrank + a.nw;
+    const uint32_t sq = hdr->s, U = hdr->U, mh_mask = hdr->mh_mask;
+    const bool qok = hdr->err == 0 && sq > 0;
+    const uint2* gitems = (const uint2*)(slot + a.L.off_items);
+    for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) qitem[i] = gitems[i];
+    for (int i = threadIdx.x; i < a.nw; i += blockDim.x) qbits[i] = 0u;
+    if (a.map) {
+        const uint2* gm = a.map + (int64_t)q * a.nw;
+        for (int i = threadIdx.x; i < a.nw; i += blockDim.x) smap[i] = gm[i];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) {
+        const uint32_t x = gitems[i].x & FTI_VOCAB_MASK;
+        atomicOr(&qbits[x >> 5], 1u << (x & 31));
+    }
+    __syncthreads();
+    {
+        __shared__ int tmp[32];
+        int run = 0;
+        for (int c0 = 0; c0 < a.nw; c0 += blockDim.x) {
+            const int w = c0 + threadIdx.x;
+            const int v = w < a.nw ? __popc(qbits[w]) : 0;
+            int tot;
+            const int r = run + fti_block_exclusive_sum(v, tmp, &tot);
+            if (w < a.nw) qrank[w] = (uint32_t)r;
+            run += tot;
+        }
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* myq = queue + warp * DCAP * 32 + lane;
+    const float* trow = a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
+    const uint32_t ld = (uint32_t)a.ld;
+    const bool smap_on = a.map != nullptr;
+    const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
+    const bool qmn = hdr->n_mn > 0;
+    unsigned ubytes = 0;
+    __shared__ unsigned long long skey[DW * 32];
+    const int64_t stride = (int64_t)gridDim.x * DW * 32;
+    for (int64_t cbase = (int64_t)blockIdx.x * DW * 32; cbase < a.n_docs; cbase += stride) {
+        // the CTA's DW*32 positions sorted by doc support size, so the lanes of a warp run merges
+        // of similar length (the warp steps until its longest pair is done)
+        {
+            const int64_t p = cbase + threadIdx.x;
+            uint32_t sz = 0xFFFFFFFFu;
+            if (p < a.n_docs) {
+                const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + p] : p;
+                sz = (doc >= 0 && doc < a.n) ? a.doc_off[doc + 1] - a.doc_off[doc] : 0u;
+            }
+            __syncthreads();   // the previous chunk's keys are consumed
+            skey[threadIdx.x] = ((unsigned long long)sz << 32) | (uint32_t)threadIdx.x;
+            __syncthreads();
+            fti_bitonic_sort_u64(skey, DW * 32);
+        }
+        const int64_t dp = cbase + (int64_t)(uint32_t)skey[threadIdx.x];
+        bool active = false;
+        int s = 0;
+        uint32_t i0 = 0, W = 0;
+        double* outp = nullptr;
+        if (dp < a.n_docs) {
+            const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
+            outp = a.out + (int64_t)q * a.out_ld + dp;
+            if (!qok || doc < 0 || doc >= a.n) {
+                // a negative candidate (padding, or a doc another shard owns) scores +inf; an invalid
+                // query or a doc index ≥ n scores NaN (as the warp kernel)
+                *outp = (qok && doc < 0) ? __longlong_as_double(0x7ff0000000000000ll)
+                                         : __longlong_as_double(0x7ff8000000000000ll);
+                if (qok && doc >= a.n) atomicOr(a.err, FTI_ERR_RANGE);
+            } else {
+                i0 = a.doc_off[doc];
+                s = (int)(a.doc_off[doc + 1] - i0);
+                W = a.Wd[doc];
+                active = true;
+                // a common M-node: the pair needs phase B — hand it to the warp kernel
+                const uint32_t m0 = a.mn_off[doc], m1 = a.mn_off[doc + 1];
+                bool general = false;
+                if (qmn) {
+                    for (uint32_t r = m0; r < m1 && !general; r++) {
+                        const uint32_t node = a.mnodes[r].x;
+                        uint32_t h = fti_hash(node) & mh_mask;
+                        while (true) {
+                            const uint32_t kk = gmh[h].x;
+                            if (kk == node) { general = true; break; }
+                            if (kk == FTI_EMPTY) break;
+                            h = (h + 1) & mh_mask;
+                        }
+                    }
+                }
+                if (general) active = false;
+            }
+        }
+        // shared ids, in vocab order: {i | j << 8 | w << 16}
+        int nc = 0;
+        if (active) {
+            for (int i = 0; i < s; i += 8) {
+                uint2 it[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) it[u] = i + u < s ? a.items[i0 + i + u] : make_uint2(0u, 0u);
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const uint32_t x = it[u].x & FTI_VOCAB_MASK;
+                    const uint32_t bw = qbits[x >> 5], bm = 1u << (x & 31);
+                    if (i + u < s && (bw & bm)) {
+                        const uint32_t j = qrank[x >> 5] + __popc(bw & (bm - 1u));
+                        if (nc < DCAP) myq[nc * 32] = (uint32_t)(i + u) | (j << 8) | (it[u].y << 16);
+                        nc++;
+                    }
+                }
+            }
+        }
+        if (active && (nc > DCAP || dp >= a.n_docs)) active = false;
+        const bool to_list = dp < a.n_docs && outp && !active && s > 0 && qok;
+        if (to_list) {
+            const uint32_t pos = atomicAdd(&a.fb_cnt[q], 1u);
+            a.fb_list[(int64_t)q * a.fb_cap + pos] = (uint32_t)dp;
+        }
+        const bool scored = active;
+        // ---- root northwest corner, lane-sequential, branch-free ----
+        // (ra, ro): residual and table-row offset of doc item i; (ran, ron) item i+1; p2 / p3 the raw
+        // records of items i+2 / i+3 (loaded two advances before use).  rb / rbn: residuals of query
+        // items j / j+1.  ed / eq: the next queued shared id for the doc / query side.
+        const uint2* dit = a.items + i0;
+        int i = 0, j = 0, cd = 0, cq = 0;
+        uint32_t ed = nc > 0 ? myq[0] : DQ_END, eq = ed;
+        uint32_t ra = 0, ro = 0, ran = 0, ron = 0, rb = 0, rbn = 0;
+        uint2 p2 = make_uint2(0u, 0u), p3 = make_uint2(0u, 0u);
+        // doc item ii from its record it: residual after its self match, and its table-row offset
+        auto doc_prep = [&](const uint2 it, int ii, bool take, uint32_t& r_, uint32_t& o_) {
+            const uint32_t x = it.x & FTI_VOCAB_MASK;
+            uint32_t m = it.y * U;
+            const bool hit = take && (ed & 0xFFu) == (uint32_t)ii;
+            const uint32_t qm = qitem[(ed >> 8) & 0xFFu].y * W;
+            const uint32_t adj = hit ? (qm < m ? qm : m) : 0u;
+            cd += hit;
+            const uint32_t ne = myq[(cd < DCAP ? cd : DCAP - 1) * 32];
+            ed = hit ? (cd < nc ? ne : DQ_END) : ed;
+            uint32_t row = x;
+            if (smap_on) {
+                const uint2 mw = smap[x >> 5];
+                row = mw.y + __popc(mw.x & ((1u << (x & 31)) - 1u));
+            }
+            r_ = m - adj;
+            o_ = row * ld;
+        };
+        // query item jj: residual after its self match
+        auto q_prep = [&](int jj, bool take) {
+            uint32_t m = qitem[jj].y * W;
+            const bool hit = take && ((eq >> 8) & 0xFFu) == (uint32_t)jj;
+            const uint32_t dm = (eq >> 16) * U;
+            const uint32_t adj = hit ? (dm < m ? dm : m) : 0u;
+            cq += hit;
+            const uint32_t ne = myq[(cq < DCAP ? cq : DCAP - 1) * 32];
+            eq = hit ? (cq < nc ? ne : DQ_END) : eq;
+            return m - adj;
+        };
+        if (active) {
+            const uint2 t0 = dit[0];
+            const uint2 t1 = s > 1 ? dit[1] : t0;
+            if (s > 2) p2 = dit[2];
+            if (s > 3) p3 = dit[3];
+            doc_prep(t0, 0, true, ra, ro);
+            doc_prep(t1, 1, s > 1, ran, ron);
+            rb = q_prep(0, true);
+            rbn = q_prep(sq > 1 ? 1 : 0, sq > 1);
+        }
+        const int sqm1 = (int)sq - 1;
+        double acc = 0.0;
+        // software pipeline: the gathers of one batch are in flight while the next batch is merged
+        float pdv[DRB];
+        uint32_t pef[DRB];
+#pragma unroll
+        for (int u = 0; u < DRB; u++) { pdv[u] = 0.f; pef[u] = 0u; }
+        while (__any_sync(0xffffffffu, active)) {
+            uint32_t off[DRB];
+            uint32_t ef[DRB];
+#pragma unroll
+            for (int u = 0; u < DRB; u++) {
+                const uint32_t eta = active ? (ra < rb ? ra : rb) : 0u;
+                off[u] = ro + (uint32_t)j;
+                ef[u] = eta;
+                ra -= eta;
+                rb -= eta;
+                const bool ad = active && ra == 0u, aq = active && rb == 0u;
+                // doc side: item i+2 (record p2) becomes the prepared next item
+                uint32_t r2, o2;
+                doc_prep(p2, i + 2, ad && i + 2 < s, r2, o2);
+                ra = ad ? ran : ra;
+                ro = ad ? ron : ro;
+                ran = ad ? r2 : ran;
+                ron = ad ? o2 : ron;
+                p2 = ad ? p3 : p2;
+                if (ad && i + 4 < s) p3 = dit[i + 4];
+                i += ad;
+                // query side: item j+2
+                const int j2 = j + 2 < (int)sq ? j + 2 : sqm1;
+                const uint32_t q2 = q_prep(j2, aq && j + 2 < (int)sq);
+                rb = aq ? rbn : rb;
+                rbn = aq ? q2 : rbn;
+                j += aq;
+                active = active && i < s && j < (int)sq;
+            }
+            float part = 0.f;
+#pragma unroll
+            for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
+            acc += (double)part;
+#pragma unroll
+            for (int u = 0; u < DRB; u++) {
+                pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
+                pef[u] = ef[u];
+            }
+        }
+        {
+            float part = 0.f;
+#pragma unroll
+            for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
+            acc += (double)part;
+        }
+        if (scored) {
+            *outp = acc / (double)((unsigned long long)W * U);
+            ubytes += 8u * (unsigned)s + 16u;
+        }
+    }
+    if (a.units) {
+        const unsigned tot = __reduce_add_sync(0xffffffffu, ubytes);
+        if (lane == 0 && tot) atomicAdd(a.units, (unsigned long long)tot);
+    }
+}
+
+}  // namespace
+
+// Lane-per-pair Flowtree over n_docs candidate positions per query (d_docs, or all docs when
+// null) with a distance table.  Pairs it cannot score are listed per query in fb_list / fb_cnt
+// (capacity n_docs per query) for the warp kernel's list mode.  cudaErrorNotSupported when the
+// geometry does not fit (supports > 255, N beyond the shared-memory bitmap).
+cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
+                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st) {
+    const ft_index* ix = ds->ix;
+    if (!tab.table || ds->max_s > 255 || L.smax > 255) return cudaErrorNotSupported;
+    DArgs a{};
+    a.nw = (int)((ix->N + 31) / 32);
+    a.Sq = std::max(1, L.smax);
+    const size_t smem = 8ull * a.Sq + (tab.map ? 8ull * a.nw : 0) + 8ull * a.nw + 4ull * DW * DCAP * 32;
+    if (smem > 200 * 1024) return cudaErrorNotSupported;
+    cudaError_t e;
+    if ((e = ds->s_fblist.reserve((size_t)nq * n_docs * 4)) != cudaSuccess) return e;
+    if ((e = ds->s_fbcnt.reserve((size_t)nq * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ds->s_fbcnt.p, 0, (size_t)nq * 4, st)) != cudaSuccess) return e;
+    a.doc_off = ds->doc_off; a.items = ds->items; a.Wd = ds->W;
+    a.mn_off = ds->mn_off; a.mnodes = ds->mnodes;
+    a.qblock = d_qblock; a.L = L;
+    a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;
+    a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.rows_cap = tab.rows_cap; a.ld = tab.ld;
+    a.out = d_out; a.out_ld = out_ld;
+    a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;
+    a.err = ds->err_dev;
+    a.units = ds->units_ptr(FTI_ST_FT);
+    if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return e;
+    const int64_t gx = (n_docs + DW * 32 - 1) / (DW * 32);
+    for (int32_t q0 = 0; q0 < nq; q0 += 65535) {
+        a.q0 = q0;
+        k_ftd<<<dim3((unsigned)gx, (unsigned)std::min(65535, nq - q0)), DW * 32, smem, st>>>(a);
+        fti_count_launches(1);
+    }
+    *fb_list = a.fb_list;
+    *fb_cnt = a.fb_cnt;
+    return cudaGetLastError();
+}

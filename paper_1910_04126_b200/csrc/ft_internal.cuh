@@ -175,6 +175,11 @@ struct FtTable {
 // exhaustive Flowtree, lane = query of a 32-query chunk (ft_flowx.cu); pairs it cannot score are
 // listed per query in *fb_list / *fb_cnt (capacity n_docs per query) for the warp kernel
 #define FTX_MAX_SQ 256
+// lane-per-pair Flowtree with a distance table (ft_flowd.cu), candidate lists or all docs; the
+// pairs it cannot score are listed the same way
+cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
+                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st);
 cudaError_t fti_launch_ftx(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t n_docs,
                            const FtTable& tab, double* d_out, int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt,
                            cudaStream_t st);

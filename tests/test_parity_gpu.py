@@ -237,6 +237,32 @@ def test_chunked_flowtree_matches_warp_kernel(ft, monkeypatch, name, nq):
     assert np.array_equal(a == 0.0, b == 0.0)
 
 
+@pytest.mark.parametrize("name,nq,mode", [("text", 40, "lists"), ("reviews", 70, "lists"), ("reviews", 9, "all"),
+                                           ("stress", 5, "lists")])
+def test_lane_per_pair_flowtree_matches_other_kernels(ft, monkeypatch, name, nq, mode):
+    """The lane-per-pair kernel (k_ftd: 32 pairs of one query per warp, pairs with a common M-node
+    or more than 32 shared ids listed for the warp kernel) against the warp kernel for every pair
+    (FT_GENERAL_ONLY=1) and, over all docs, the lane-per-query chunk kernel (FT_FTX=1).  Candidate
+    lists (mode "lists") hold repeats and a ragged tail, as the pipeline's top-m rows do."""
+    wl = get_workload(name, n_docs=3000, n_queries=nq)
+    ix, ds = _setup(ft, wl)
+    docs = None
+    if mode == "lists":
+        rng = np.random.default_rng(5)
+        docs = np.concatenate([rng.choice(wl.n, 700, replace=False), [0, wl.n - 1, 0]]).astype(np.int64)
+    a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
+    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
+    monkeypatch.delenv("FT_GENERAL_ONLY")
+    assert np.all(np.isfinite(a))
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
+    assert np.array_equal(a == 0.0, b == 0.0)
+    if mode == "all":
+        monkeypatch.setenv("FT_FTX", "1")
+        c = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+        np.testing.assert_allclose(a, c, rtol=1e-6, atol=0)
+
+
 @pytest.mark.parametrize("name", ["image", "text", "reviews"])
 def test_qt_dense_matches_hash(ft, monkeypatch, name):
     """The Quadtree kernel scans a chunk with the dense bitmap structure when its node union is
