@@ -24,9 +24,18 @@
 
 namespace {
 
+#ifndef FTD_MINB
+#define FTD_MINB 3         // CTAs per SM the register budget allows
+#endif
+#ifndef FTD_DCAP
+#define FTD_DCAP 32
+#endif
 constexpr int DW = 8;      // warps per CTA
-constexpr int DCAP = 32;   // shared ids per pair held in the per-lane queue
-constexpr int DRB = 8;     // merge steps per gather batch
+constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
+#ifndef FTD_DRB
+#define FTD_DRB 8
+#endif
+constexpr int DRB = FTD_DRB;   // merge steps per gather batch
 constexpr uint32_t DQ_END = 0xFFFFFFFFu;   // queue sentinel: i = j = 255 never matches (s, sq ≤ 255)
 
 struct DArgs {
@@ -55,7 +64,7 @@ struct DArgs {
     unsigned long long* units;
 };
 
-__global__ void __launch_bounds__(DW * 32, 2) k_ftd(DArgs a) {
+__global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int q = a.q0 + (int)blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;

@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflowtree_b200.so")
+# FT_LIB (development hook, tools/variants.py): an alternative build of the same library
+LIB_PATH = os.environ.get("FT_LIB") or os.path.join(_HERE, "libflowtree_b200.so")
 
 FT_OK, FT_EINVAL, FT_ERANGE, FT_EOVERFLOW, FT_ENOMEM, FT_ECUDA, FT_ESTATE = range(7)
 STATUS_NAMES = {0: "FT_OK", 1: "FT_EINVAL", 2: "FT_ERANGE", 3: "FT_EOVERFLOW", 4: "FT_ENOMEM",

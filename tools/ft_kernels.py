@@ -23,7 +23,10 @@ si = torch.from_numpy(sub.q_ids).cuda()
 sw = torch.from_numpy(sub.q_w.view(np.int32)).cuda().view(torch.uint32)
 out = torch.empty((sub.nq, wl.n), dtype=torch.float64, device="cuda")
 res = {}
+only = sys.argv[4].split(",") if len(sys.argv) > 4 else None
 for var, env in (("ftd", {}), ("ftx", {"FT_FTX": "1"}), ("warp", {"FT_GENERAL_ONLY": "1"})):
+    if only and var not in only:
+        continue
     for k in ("FT_FTX", "FT_GENERAL_ONLY"):
         os.environ.pop(k, None)
     os.environ.update(env)
@@ -50,7 +53,7 @@ for var, env in (("ftd", {}), ("ftx", {"FT_FTX": "1"}), ("warp", {"FT_GENERAL_ON
           f"({sub.nq} q x {wl.n} docs = {sub.nq * wl.n / ex / 1e6:.3f} G pairs/s); dist {p.get('dist_table', (0,))[0]/3:.3f} ms",
           flush=True)
 a = res["ftd"][2]
-for v in ("ftx", "warp"):
+for v in [v for v in ("ftx", "warp") if v in res]:
     b = res[v][2]
     print(v, "max rel diff vs ftd", float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))),
           "knn ids equal", bool(np.array_equal(res[v][3], res["ftd"][3])))
