@@ -7,7 +7,7 @@
 //   * M-nodes: a cell with ≥ 2 ground points present on both sides (phase B of the warp kernel)
 //     hands the pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
 //   * self matches (reading R8): one pass over the doc items tests the query bitmap and queues
-//     the shared ids {doc index i, query index j, w} in increasing vocab order, so both sides of
+//     the shared ids {doc index i, query index j} in increasing vocab order, so both sides of
 //     the merge below consume the queue with a monotone cursor;
 //   * root: the northwest corner over the residuals in vocab order (reading R10) as a sequential
 //     two-pointer — η = min of the current residuals, the exhausted side advances — with the next
@@ -36,7 +36,7 @@ constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane que
 #define FTD_DRB 8
 #endif
 constexpr int DRB = FTD_DRB;   // merge steps per gather batch
-constexpr uint32_t DQ_END = 0xFFFFFFFFu;   // queue sentinel: i = j = 255 never matches (s, sq ≤ 255)
+constexpr uint32_t DQ_END = 0xFFFFu;   // queue sentinel: i = j = 255 never matches (s, sq ≤ 255)
 
 struct DArgs {
     const uint32_t* doc_off;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     uint2* smap = qitem + a.Sq;
     uint32_t* qbits = (uint32_t*)(smap + (a.map ? a.nw : 0));
     uint32_t* qrank = qbits + a.nw;
-    uint32_t* queue = qrank + a.nw;
+    uint16_t* queue = (uint16_t*)(qrank + a.nw);
     const uint32_t sq = hdr->s, U = hdr->U, mh_mask = hdr->mh_mask;
     const bool qok = hdr->err == 0 && sq > 0;
     const uint2* gitems = (const uint2*)(slot + a.L.off_items);
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* myq = queue + warp * DCAP * 32 + lane;
+    uint16_t* myq = queue + warp * DCAP * 32 + lane;
     const float* trow = a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
     const uint32_t ld = (uint32_t)a.ld;
     const bool smap_on = a.map != nullptr;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     const uint32_t bw = qbits[x >> 5], bm = 1u << (x & 31);
                     if (i + u < s && (bw & bm)) {
                         const uint32_t j = qrank[x >> 5] + __popc(bw & (bm - 1u));
-                        if (nc < DCAP) myq[nc * 32] = (uint32_t)(i + u) | (j << 8) | (it[u].y << 16);
+                        if (nc < DCAP) myq[nc * 32] = (uint16_t)((uint32_t)(i + u) | (j << 8));
                         nc++;
                     }
                 }
@@ -195,10 +195,13 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
         // ---- root northwest corner, lane-sequential, branch-free ----
         // (ra, ro): residual and table-row offset of doc item i; (ran, ron) item i+1; p2 / p3 the raw
         // records of items i+2 / i+3 (loaded two advances before use).  rb / rbn: residuals of query
-        // items j / j+1.  ed / eq: the next queued shared id for the doc / query side.
+        // items j / j+1.  ed / eq: the next queued shared id {i | j << 8} for the doc / query side;
+        // eqw the doc weight of eq's item (loaded when eq is set, used at the query side's next hit).
         const uint2* dit = a.items + i0;
+        const uint32_t* dw = (const uint32_t*)dit + 1;   // weights, stride 2 words
         int i = 0, j = 0, cd = 0, cq = 0;
-        uint32_t ed = nc > 0 ? myq[0] : DQ_END, eq = ed;
+        uint32_t ed = nc > 0 ? (uint32_t)myq[0] : DQ_END, eq = ed, eqw = 0u;
+        if (nc > 0) eqw = dw[2 * (eq & 0xFFu)];
         uint32_t ra = 0, ro = 0, ran = 0, ron = 0, rb = 0, rbn = 0;
         uint2 p2 = make_uint2(0u, 0u), p3 = make_uint2(0u, 0u);
         // doc item ii from its record it: residual after its self match, and its table-row offset
@@ -223,11 +226,12 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
         auto q_prep = [&](int jj, bool take) {
             uint32_t m = qitem[jj].y * W;
             const bool hit = take && ((eq >> 8) & 0xFFu) == (uint32_t)jj;
-            const uint32_t dm = (eq >> 16) * U;
+            const uint32_t dm = eqw * U;
             const uint32_t adj = hit ? (dm < m ? dm : m) : 0u;
             cq += hit;
             const uint32_t ne = myq[(cq < DCAP ? cq : DCAP - 1) * 32];
             eq = hit ? (cq < nc ? ne : DQ_END) : eq;
+            if (hit && cq < nc) eqw = dw[2 * (eq & 0xFFu)];
             return m - adj;
         };
         if (active) {
@@ -317,7 +321,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     DArgs a{};
     a.nw = (int)((ix->N + 31) / 32);
     a.Sq = std::max(1, L.smax);
-    const size_t smem = 8ull * a.Sq + (tab.map ? 8ull * a.nw : 0) + 8ull * a.nw + 4ull * DW * DCAP * 32;
+    const size_t smem = 8ull * a.Sq + (tab.map ? 8ull * a.nw : 0) + 8ull * a.nw + 2ull * DW * DCAP * 32;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     cudaError_t e;
     if ((e = ds->s_fblist.reserve((size_t)nq * n_docs * 4)) != cudaSuccess) return e;
@@ -334,6 +338,17 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.units = ds->units_ptr(FTI_ST_FT);
     if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
+    // the L1 caches the lanes' doc records between the pre-pass and the merge: give shared memory
+    // only what the target CTAs per SM need (3, or 2 with the 25 KB-class candidate row map)
+    {
+        const int ctas = tab.map ? 2 : FTD_MINB;
+        const size_t need = (size_t)ctas * (smem + 2176 + 1024);
+        int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+        if (const char* ev = getenv("FT_FTD_CARVEOUT")) pct = atoi(ev);
+        if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct))) !=
+            cudaSuccess)
+            return e;
+    }
     const int64_t gx = (n_docs + DW * 32 - 1) / (DW * 32);
     for (int32_t q0 = 0; q0 < nq; q0 += 65535) {
         a.q0 = q0;
