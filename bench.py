@@ -237,7 +237,7 @@ def run_b200(args):
     alg_bytes = {"quadtree": qt_bytes * stages["quadtree"][1], "dist_table": units["dist_table"],
                  "flowtree": units["flowtree"]}
     kern = {"quadtree": "k_qt (Quadtree estimate, a3)", "dist_table": "k_dist_tc (tcgen05 distance table, a5)",
-            "flowtree": "k_flowtree (Flowtree estimate, a6)"}
+            "flowtree": "k_ftd (lane-per-pair Flowtree estimate, a6) + k_flowtree (list mode: pairs sharing an M-node)"}
     traffic_all = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):

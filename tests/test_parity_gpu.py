@@ -223,7 +223,7 @@ def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
 
 @pytest.mark.parametrize("name,nq", [("text", 40), ("reviews", 70)])
 def test_chunked_flowtree_matches_warp_kernel(ft, monkeypatch, name, nq):
-    """Exhaustive scoring runs the lane-per-query chunk kernel (pairs sharing an M-node are listed
+    """Exhaustive scoring runs the lane-per-pair kernel k_ftd (pairs sharing an M-node are listed
     for the warp kernel); FT_GENERAL_ONLY=1 runs the warp kernel for every pair.  The flows are the
     same triples, so the values agree to FP summation order; ragged chunks (nq not a multiple of
     32) included."""

@@ -15,19 +15,14 @@ $Q > gpurun_out/kp_qt.log 2>&1 && \
 echo "qt rc=$?"
 K="python tools/kprof.py knn --queries 1000 --reps 1"
 $K > gpurun_out/kp_knn.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_dist_tc|k_flowtree|k_select_fast|k_vocab|k_qt_dense|k_tiles|k_dist_prep|k_tile_plan" -c 8 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_dist_tc|k_ftd|k_flowtree|k_select_fast|k_vocab|k_qt_dense|k_tiles|k_dist_prep|k_tile_plan" -c 9 \
   -o gpurun_out/prof_knn $K > gpurun_out/ncu_knn.log 2>&1
 echo "knn rc=$?"
-F="python tools/kprof.py ft --queries 16 --reps 1"
-$F > gpurun_out/kp_ft.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_flowtree" -c 1 -o gpurun_out/prof_ft $F \
-  > gpurun_out/ncu_ft.log 2>&1
-echo "ft rc=$?"
 X="python tools/kprof.py ft --queries 64 --reps 1"
-$X > gpurun_out/kp_ftx.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_ftx$" -c 1 -o gpurun_out/prof_ftx $X \
-  > gpurun_out/ncu_ftx.log 2>&1
-echo "ftx rc=$?"
+$X > gpurun_out/kp_ftd.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ftd|k_flowtree" -c 2 -o gpurun_out/prof_ftd $X \
+  > gpurun_out/ncu_ftd.log 2>&1
+echo "ftd rc=$?"
 E="python tools/kprof.py exact --queries 1000 --reps 1"
 $E > gpurun_out/kp_exact.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_exact" -c 1 -o gpurun_out/prof_exact $E \

@@ -68,8 +68,7 @@ traffic = {}
 summ = [f"# {rnd}: key metrics from `ncu --set full --clock-control none` (tools/profile_round.sh)", ""]
 for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one k_qt launch = 1e8 pairs)"),
                   ("prof_knn.ncu-rep", "kprof knn --queries 1000 (the bench batch: one launch of each kernel per step)"),
-                  ("prof_ft.ncu-rep", "kprof ft --queries 16 (exhaustive Flowtree over 100k docs)"),
-                  ("prof_ftx.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree, lane-per-query chunk kernel k_ftx)"),
+                  ("prof_ftd.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree over 100k docs: k_ftd + list-mode k_flowtree)"),
                   ("prof_exact.ncu-rep", "kprof exact --queries 1000 (QT 424 -> FT 9 -> exact W1, transportation simplex)")]:
     p = os.path.join(OUT, rep)
     if not os.path.exists(p):
@@ -80,19 +79,22 @@ for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one
         summ.append(f"### {short}")
         for m, (v, u) in ms.items():
             summ.append(f"  {m} = {v} {u}")
+        # the Flowtree stage is k_ftd plus the list-mode k_flowtree: their traffic is summed
         key = {("k_qt", "prof_qt.ncu-rep"): "quadtree", ("k_dist_tc", "prof_knn.ncu-rep"): "dist_table",
-               ("k_flowtree", "prof_knn.ncu-rep"): "flowtree"}.get((short.split("<")[0], rep))
-        if key and f"{key}_dram_bytes_per_launch" not in traffic:
+               ("k_ftd", "prof_knn.ncu-rep"): "flowtree", ("k_flowtree", "prof_knn.ncu-rep"): "flowtree"}.get(
+            (short.split("<")[0], rep))
+        if key:
             rd = float(ms["dram__bytes_read.sum"][0].replace(",", ""))
             wr = float(ms["dram__bytes_write.sum"][0].replace(",", ""))
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            traffic[f"{key}_dram_bytes_per_launch"] = rd * scale.get(ms["dram__bytes_read.sum"][1], 1) + \
+            kk = f"{key}_dram_bytes_per_launch"
+            traffic[kk] = traffic.get(kk, 0.0) + rd * scale.get(ms["dram__bytes_read.sum"][1], 1) + \
                 wr * scale.get(ms["dram__bytes_write.sum"][1], 1)
         summ.append("")
 open(os.path.join(PROF, f"{rnd}_ncu_summary.txt"), "w").write("\n".join(summ) + "\n")
 if traffic:
     traffic["source"] = (f"profiles/{rnd}_ncu_summary.txt: dram read+write of one ncu --set full launch (k_qt: the "
-                         "1000-query bench batch; k_dist_tc / k_flowtree: kprof knn on the same 1000-query batch, "
-                         "one launch each, as in the bench)")
+                         "1000-query bench batch; k_dist_tc / k_ftd + k_flowtree: kprof knn on the same 1000-query "
+                         "batch, one launch each, as in the bench)")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     print(traffic)
