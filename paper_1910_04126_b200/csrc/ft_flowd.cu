@@ -4,8 +4,9 @@
 // A CTA works for one query: its items, its vocab bitmap + per-word rank (query item index of an
 // id) and, for a compact candidate table, its row map ({bits, rank} per 32 vocab ids) sit in
 // shared memory.  Lane l of a warp scores the pair (q, docs[base + l]) on its own:
-//   * M-nodes: a cell with ≥ 2 ground points present on both sides (phase B of the warp kernel)
-//     hands the pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
+//   * M-nodes: a cell with ≥ 2 ground points present on both sides where both keep residual mass
+//     after the leaves' self matches (so phase B of the warp kernel would match there) hands the
+//     pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
 //   * self matches (reading R8): one pass over the doc items tests the query bitmap and queues
 //     the shared ids {doc index i, query index j} in increasing vocab order, so both sides of
 //     the merge below consume the queue with a monotone cursor;
@@ -44,6 +45,7 @@ struct DArgs {
     const uint32_t* Wd;
     const uint32_t* mn_off;
     const uint4* mnodes;
+    const uint16_t* mlists;
     const uint8_t* qblock;
     QueryLayout L;
     int32_t q0;
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const uint32_t ld = (uint32_t)a.ld;
     const bool smap_on = a.map != nullptr;
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
+    const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
     const bool qmn = hdr->n_mn > 0;
     unsigned ubytes = 0;
     __shared__ unsigned long long skey[DW * 32];
@@ -134,8 +137,9 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
         int s = 0;
         uint32_t i0 = 0, W = 0;
         double* outp = nullptr;
+        int64_t doc = -1;
         if (dp < a.n_docs) {
-            const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
+            doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
             outp = a.out + (int64_t)q * a.out_ld + dp;
             if (!qok || doc < 0 || doc >= a.n) {
                 // a negative candidate (padding, or a doc another shard owns) scores +inf; an invalid
@@ -148,22 +152,6 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                 s = (int)(a.doc_off[doc + 1] - i0);
                 W = a.Wd[doc];
                 active = true;
-                // a common M-node: the pair needs phase B — hand it to the warp kernel
-                const uint32_t m0 = a.mn_off[doc], m1 = a.mn_off[doc + 1];
-                bool general = false;
-                if (qmn) {
-                    for (uint32_t r = m0; r < m1 && !general; r++) {
-                        const uint32_t node = a.mnodes[r].x;
-                        uint32_t h = fti_hash(node) & mh_mask;
-                        while (true) {
-                            const uint32_t kk = gmh[h].x;
-                            if (kk == node) { general = true; break; }
-                            if (kk == FTI_EMPTY) break;
-                            h = (h + 1) & mh_mask;
-                        }
-                    }
-                }
-                if (general) active = false;
             }
         }
         // shared ids, in vocab order: {i | j << 8 | w << 16}
@@ -185,7 +173,60 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                 }
             }
         }
-        if (active && (nc > DCAP || dp >= a.n_docs)) active = false;
+        if (active && nc > DCAP) active = false;
+        // M-nodes (cells holding ≥ 2 ground points) on both sides: matching happens at such a node v
+        // only if, after the self matches at the leaves, both sides keep residual mass under v.  When
+        // no common M-node does, phase B changes nothing and the pair is a leaves + root flow; else
+        // the pair goes to the warp kernel.  (If no node matches, the residuals each node sees are
+        // the self-match residuals, so testing every node against them is exact.)
+        if (active && qmn) {
+            const uint32_t m0 = a.mn_off[doc], m1 = a.mn_off[doc + 1];
+            const uint32_t* dw = (const uint32_t*)(a.items + i0) + 1;
+            bool general = false;
+            for (uint32_t r = m0; r < m1 && !general; r++) {
+                const uint4 rec = a.mnodes[r];
+                uint32_t h = fti_hash(rec.x) & mh_mask;
+                uint4 qe = make_uint4(FTI_EMPTY, 0u, 0u, 0u);
+                while (true) {
+                    const uint4 e = gmh[h];
+                    if (e.x == rec.x || e.x == FTI_EMPTY) { qe = e; break; }
+                    h = (h + 1) & mh_mask;
+                }
+                if (qe.x != rec.x) continue;
+                uint32_t dsum = 0u, qsum = 0u;
+                bool multi_shared = false;
+                for (uint32_t t = 0; t < rec.z; t++) {
+                    const uint32_t ii = a.mlists[rec.y + t];
+                    const uint32_t xv = a.items[i0 + ii].x;
+                    const uint32_t x = xv & FTI_VOCAB_MASK;
+                    uint32_t m = dw[2 * ii] * U;
+                    const uint32_t bw = qbits[x >> 5], bm = 1u << (x & 31);
+                    if (bw & bm) {
+                        // a shared id whose leaf holds ≥ 2 points is matched by that leaf's northwest
+                        // corner, not by a self match: always the warp kernel
+                        multi_shared |= (xv & FTI_FLAG_MULTI_LEAF) != 0u;
+                        const uint32_t qm = qitem[qrank[x >> 5] + __popc(bw & (bm - 1u))].y * W;
+                        m -= (qm < m ? qm : m);
+                    }
+                    dsum += m;
+                }
+                for (uint32_t t = 0; t < qe.z && dsum && !multi_shared; t++) {
+                    const uint32_t jj = gml[qe.y + t];
+                    uint32_t m = qitem[jj].y * W;
+                    for (int c = 0; c < nc; c++) {
+                        const uint32_t e = myq[c * 32];
+                        if ((e >> 8) == jj) {
+                            const uint32_t dm = dw[2 * (e & 0xFFu)] * U;
+                            m -= (dm < m ? dm : m);
+                            break;
+                        }
+                    }
+                    qsum += m;
+                }
+                general = multi_shared || (dsum > 0u && qsum > 0u);
+            }
+            if (general) active = false;
+        }
         const bool to_list = dp < a.n_docs && outp && !active && s > 0 && qok;
         if (to_list) {
             const uint32_t pos = atomicAdd(&a.fb_cnt[q], 1u);
@@ -328,7 +369,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     if ((e = ds->s_fbcnt.reserve((size_t)nq * 4)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(ds->s_fbcnt.p, 0, (size_t)nq * 4, st)) != cudaSuccess) return e;
     a.doc_off = ds->doc_off; a.items = ds->items; a.Wd = ds->W;
-    a.mn_off = ds->mn_off; a.mnodes = ds->mnodes;
+    a.mn_off = ds->mn_off; a.mnodes = ds->mnodes; a.mlists = ds->mlists;
     a.qblock = d_qblock; a.L = L;
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;
     a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.rows_cap = tab.rows_cap; a.ld = tab.ld;

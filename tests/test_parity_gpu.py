@@ -263,6 +263,29 @@ def test_lane_per_pair_flowtree_matches_other_kernels(ft, monkeypatch, name, nq,
         np.testing.assert_allclose(a, c, rtol=1e-6, atol=0)
 
 
+@pytest.mark.parametrize("max_depth", [1, 2])
+def test_lane_per_pair_flowtree_capped_tree(ft, monkeypatch, max_depth):
+    """A depth cap that binds (d = 300 mixture, D = 1 or 2) puts many points into multi-point
+    leaves and M-nodes: the lane-per-pair kernel must hand every pair whose flow matches at an
+    M-node (or at a multi-point leaf holding a shared id) to the warp kernel and score the rest as
+    leaves + root.  Against the warp kernel for every pair and, sampled, the oracle."""
+    import dataclasses
+    wl = dataclasses.replace(get_workload("reviews", n_docs=2000, n_queries=6), max_depth=max_depth)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    rng = np.random.default_rng(3)
+    docs = rng.choice(wl.n, 600, replace=False).astype(np.int64)
+    a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
+    full = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
+    fb = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
+    np.testing.assert_allclose(full, fb, rtol=1e-6, atol=0)
+    pairs = [(q, int(d)) for q in range(wl.nq) for d in rng.choice(wl.n, 25, replace=False)]
+    assert_ft_close([full[q, d] for q, d in pairs], _oracle_all(T, wl, "ft", pairs), f"capped D={max_depth}")
+
+
 @pytest.mark.parametrize("name", ["image", "text", "reviews"])
 def test_qt_dense_matches_hash(ft, monkeypatch, name):
     """The Quadtree kernel scans a chunk with the dense bitmap structure when its node union is
