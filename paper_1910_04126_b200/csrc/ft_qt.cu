@@ -319,6 +319,7 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
 // (per-word prefix + popc), and the chunk's masses are a dense [union][32 lanes] u16 array — a
 // query without the node reads 0 — so every hit costs one conflict-free LDS per lane, no mask
 // test, no posting search.  The node's depth rides in the doc record (mass | depth << 16).
+template <bool WIDE>
 __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* __restrict__ bits,
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
                                               uint4* __restrict__ hq, const ChunkHdr& sh, int nqc) {
@@ -339,11 +340,15 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
         const uint32_t W32 = a.W[doc];
         const unsigned long long A = a.A[doc];
         unsigned long long acc = 0;
-        auto term = [&](uint32_t mnu, uint32_t mmu, uint32_t sh_) {
-            // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation
+        auto term = [&](uint32_t mnu, uint32_t mmu, uint32_t f_) {
+            // U·m_μ and W·m_ν are < 2^32 (W, U ≤ 65535): 32-bit products, 64-bit accumulation.
+            // f_ = ω(v) = 2^{D* − depth}: one wide multiply-add when D* ≤ 31, else a shift
             const uint32_t um = U32 * mmu;
             const uint32_t wm = W32 * mnu;
-            acc += (unsigned long long)(um < wm ? um : wm) << sh_;
+            if (WIDE)
+                acc += (unsigned long long)(um < wm ? um : wm) << f_;
+            else
+                acc += (unsigned long long)(um < wm ? um : wm) * f_;
         };
         for (uint32_t rb = r0; rb < r1; rb += 32) {
             const uint32_t r = rb + lane;
@@ -361,7 +366,10 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             const int nh = __popc(hm);
             // the compacting lane decodes the record once: every lane then reads a ready entry
             if (id >= 0)
-                hq[__popc(hm & lt)] = make_uint4((uint32_t)id * QT_QC, y & 0xFFFFu, (uint32_t)(a.d_star - (int)(y >> 16)), 0u);
+                hq[__popc(hm & lt)] = make_uint4((uint32_t)id * QT_QC, y & 0xFFFFu,
+                                                 WIDE ? (uint32_t)(a.d_star - (int)(y >> 16))
+                                                      : 1u << (a.d_star - (int)(y >> 16)),
+                                                 0u);
             if (nh & 1) {
                 if (lane == 0) hq[nh] = make_uint4(0u, 0u, 0u, 0u);      // pad: mass 0 contributes 0
             }
@@ -469,7 +477,10 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
         for (int i = threadIdx.x; i < nwords; i += blockDim.x) sm[i] = gb[i];
         uint4* hq = (uint4*)(sm + ((2 * a.dg.mw + a.dg.cap * QT_QC / 2 + 3) & ~3));   // per-warp hit queues
         __syncthreads();
-        qt_scan_dense(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
+        if (a.d_star > 31)
+            qt_scan_dense<true>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
+        else
+            qt_scan_dense<false>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
         return;
     }
     const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
