@@ -203,11 +203,16 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     // (test hooks for the chunk boundaries).
     const size_t nwords = (size_t)(ix->N + 31) / 32;
     const size_t per_q = (size_t)rows_cap * ld * 4;
-    size_t budget = (size_t)3 << 30;
-    {
+    // the budget is fixed at the dataset's first Flowtree call: cudaMemGetInfo on every call showed
+    // as occasional multi-ms host stalls (the query is not free), and a stable budget keeps the
+    // table allocation from changing size between calls
+    if (ds->table_budget == 0) {
         size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::max(budget, std::min(fr / 4, (size_t)48 << 30));
+        ds->table_budget = (size_t)3 << 30;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+            ds->table_budget = std::max(ds->table_budget, std::min(fr / 4, (size_t)48 << 30));
     }
+    size_t budget = ds->table_budget;
     if (const char* eb = getenv("FT_TABLE_BUDGET_GB")) budget = (size_t)atoi(eb) << 30;
     int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
     if (const char* ev = getenv("FT_TABLE_CHUNK")) qch = std::max(1, std::min(qch, atoi(ev)));

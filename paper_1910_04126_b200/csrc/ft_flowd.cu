@@ -377,8 +377,13 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;
     a.err = ds->err_dev;
     a.units = ds->units_ptr(FTI_ST_FT);
-    if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-        return e;
+    // function attributes are set only when they change
+    static int cur_smem = -1, cur_pct = -1;
+    if ((int)smem > cur_smem) {
+        if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return e;
+        cur_smem = (int)smem;
+    }
     // the L1 caches the lanes' doc records between the pre-pass and the merge: give shared memory
     // only what the target CTAs per SM need (3, or 2 with the 25 KB-class candidate row map)
     {
@@ -386,9 +391,12 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
         const size_t need = (size_t)ctas * (smem + 2176 + 1024);
         int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
         if (const char* ev = getenv("FT_FTD_CARVEOUT")) pct = atoi(ev);
-        if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct))) !=
-            cudaSuccess)
-            return e;
+        pct = std::min(100, pct);
+        if (pct != cur_pct) {
+            if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess)
+                return e;
+            cur_pct = pct;
+        }
     }
     const int64_t gx = (n_docs + DW * 32 - 1) / (DW * 32);
     for (int32_t q0 = 0; q0 < nq; q0 += 65535) {

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -50,6 +52,7 @@ struct DevBuf {
         p = nullptr;
         bytes = 0;
         size_t nb = b < 256 ? 256 : b;
+        if (getenv("FT_ALLOC_DBG")) fprintf(stderr, "ft DevBuf grow -> %zu bytes\n", nb);
         cudaError_t e = cudaMalloc(&p, nb);
         if (e == cudaSuccess) bytes = nb;
         return e;
@@ -137,6 +140,7 @@ struct ft_dataset {
     uint2* qt = nullptr;
     unsigned long long* A = nullptr;  // [n] Σ_v ω(v) m_μ(v)
     int64_t n_qt = 0;
+    size_t table_budget = 0;       // a5 table bytes per query chunk (set at the first Flowtree call)
     // sticky device-side error word (FTI_ERR_* bits)
     uint32_t* err_dev = nullptr;
     // per-stage profiling (ft_profile_*)
