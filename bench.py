@@ -46,6 +46,18 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def tf32_peak_tflops():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    ratio = 1.1 / 2.25          # B200_PROFILING.md nominal dense tf32 / bf16
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        if "bf16_tflops_sustained" in j:
+            return (float(j["bf16_tflops_sustained"]) * ratio,
+                    "measured bf16 sustained (MEASURED_PEAKS.json) x nominal tf32/bf16 ratio 1.1/2.25")
+    return 1100.0, "fallback (B200_PROFILING.md 1.1 PFLOP/s dense tf32)"
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
@@ -221,7 +233,8 @@ def run_b200(args):
     ds.synchronize(stream)
     t_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     stages = ft.profile_dict(ds.h)
-    units = {"dist_table": ft.ft_profile_units(ds.h, 4), "flowtree": ft.ft_profile_units(ds.h, 5)}
+    units = {"dist_table": ft.ft_profile_units(ds.h, 4), "flowtree": ft.ft_profile_units(ds.h, 5),
+             "dist_flops": ft.ft_profile_units(ds.h, ft.FT_PROF_DIST_FLOPS)}
     ft.ft_profile_enable(ds.h, False)
     t_ms = parallel.max_over_ranks(t_ms, dist, dev)
     jobq = Q if docs_mode else world * Q                 # queries the whole job answers per step
@@ -260,7 +273,20 @@ def run_b200(args):
         rq = rooflines["quadtree"]
         rq["note"] = "per-pair algorithmic bytes (record per pair, SURVEY 8(d)); records are read once per 32 queries"
         rq["frac_chunk_amortised"] = rq["frac"] / 32.0
-    dom = max(rooflines, key=lambda s: stages[s][0])
+    if "dist_table" in rooflines and units["dist_flops"] > 0:
+        # the distance table is a contraction: its tensor roofline beside the byte one.  TF32 peak =
+        # the measured bf16 sustained peak x the guide's nominal tf32/bf16 ratio (1.1 / 2.25 PF)
+        tf32_peak, tf32_src = tf32_peak_tflops()
+        ms_d, n_d = stages["dist_table"]
+        ach_t = units["dist_flops"] / (ms_d / 1e3) / 1e12
+        rooflines["dist_table_tensor"] = {
+            "bound": "tensor", "kernel": kern["dist_table"], "achieved": ach_t, "peak": tf32_peak,
+            "unit": "TFLOP/s", "frac": ach_t / tf32_peak, "traffic": None,
+            "algorithmic_flops_per_launch": units["dist_flops"] / n_d, "launch_ms": ms_d / n_d,
+            "launches": n_d, "peak_source": tf32_src,
+            "note": "algorithmic flops 2*rows*s_q*d; the 3xTF32 kernel issues three MMA products per entry "
+                    "(plus row/column padding), so the tensor pipe executes >= 3x these"}
+    dom = max([s for s in rooflines if s in stages], key=lambda s: stages[s][0])
     roofline = dict(rooflines[dom], dominant_stage=dom)
 
     # ---- kernel-level numbers over all n docs (separately timed; not part of the step) ----

@@ -160,7 +160,10 @@ ft_status ft_profile_reset(ft_dataset* ds);
 ft_status ft_profile_read(ft_dataset* ds, int32_t stage, double* total_ms, int64_t* launches);
 /* Algorithmic bytes the kernels of a stage moved since the last reset (SURVEY §8(d) units),
  * counted on the device while profiling is enabled: stage 4 (distance table) Σ rows·(4d + 4 s_q),
- * stage 5 (Flowtree) Σ pairs·(8 s_doc + 16).  Synchronises the device.                        */
+ * stage 5 (Flowtree) Σ pairs·(8 s_doc + 16).  The extra slot FT_PROF_DIST_FLOPS holds the
+ * distance table's algorithmic flops Σ 2·rows·s_q·d (one product per entry; the
+ * 3xTF32 kernel executes three).  Synchronises the device.                                     */
+#define FT_PROF_DIST_FLOPS FT_NUM_STAGES
 ft_status ft_profile_units(ft_dataset* ds, int32_t stage, uint64_t* bytes);
 const char* ft_profile_stage_name(int32_t stage);
 uint64_t ft_launch_count(void);

@@ -508,13 +508,13 @@ extern "C" ft_status ft_profile_reset(ft_dataset* ds) {
     ft_status rc = profile_drain(ds);
     for (int s = 0; s < FT_NUM_STAGES; s++) { ds->prof_ms[s] = 0; ds->prof_n[s] = 0; }
     FTI_CUDA(cudaDeviceSynchronize());
-    FTI_CUDA(cudaMemset(ds->prof_units, 0, sizeof(unsigned long long) * FT_NUM_STAGES));
+    FTI_CUDA(cudaMemset(ds->prof_units, 0, sizeof(unsigned long long) * (FT_NUM_STAGES + 1)));
     return rc;
 }
 
 extern "C" ft_status ft_profile_units(ft_dataset* ds, int32_t stage, uint64_t* bytes) {
     if (!ds || !bytes) return fti_fail(FT_ESTATE, "ft_profile_units: NULL argument");
-    if (stage < 0 || stage >= FT_NUM_STAGES) return fti_fail(FT_EINVAL, "ft_profile_units: bad stage");
+    if (stage < 0 || stage > FT_PROF_DIST_FLOPS) return fti_fail(FT_EINVAL, "ft_profile_units: bad stage");
     FTI_CUDA(cudaDeviceSynchronize());
     unsigned long long v = 0;
     FTI_CUDA(cudaMemcpy(&v, ds->prof_units + stage, sizeof(v), cudaMemcpyDeviceToHost));

@@ -489,11 +489,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
 // Per column block: every query's MMA width N_q (its columns in this block rounded up to 16; 0 when
 // it has none), the offset of its pre-split B chunks, and the work list's tile prefix (queries
 // without columns get no tiles).  One CTA, block-wide scans over 1024-query slabs.  With `units`:
-// adds the stage's algorithmic bytes Σ_q rows_q · (4 d [first block only] + 4 s_q,block).
+// adds the stage's algorithmic bytes Σ_q rows_q · (4 d [first block only] + 4 s_q,block), and in
+// the next slot its algorithmic flops Σ_q 2 · rows_q · s_q,block · d.
 __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned long long* units) {
     __shared__ int tmp_t[32], tmp_b[32];
     int64_t tacc = 0, bacc = 0;
-    unsigned long long bytes = 0;
+    unsigned long long bytes = 0, flops = 0;
     for (int q0 = 0; q0 < a.nq; q0 += blockDim.x) {
         const int q = q0 + threadIdx.x;
         int np = 0, tiles = 0, nb = 0;
@@ -513,7 +514,10 @@ __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned 
         if (q < a.nq) {
             a.tile_base[q] = tacc + tex;
             a.qinfo[q] = make_uint2((uint32_t)(bacc + bex), (uint32_t)np);
-            if (np) bytes += (unsigned long long)r * ((a.cb == 0 ? 4ull * d : 0ull) + 4ull * nb);
+            if (np) {
+                bytes += (unsigned long long)r * ((a.cb == 0 ? 4ull * d : 0ull) + 4ull * nb);
+                flops += 2ull * (unsigned long long)r * (unsigned long long)nb * (unsigned long long)d;
+            }
         }
         tacc += tt;
         bacc += bt;
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned 
     }
     if (threadIdx.x == 0) a.tile_base[a.nq] = tacc;
     if (units && bytes) atomicAdd(units, bytes);
+    if (units && flops) atomicAdd(units + (FT_PROF_DIST_FLOPS - FTI_ST_DIST), flops);
 }
 
 // grid (nq, slices): the tiles' descriptors and row ids

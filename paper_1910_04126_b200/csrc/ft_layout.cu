@@ -354,8 +354,8 @@ extern "C" ft_status ft_load_dataset(const ft_index* ix, const int64_t* doc_off,
     cudaStreamDestroy(st);
     FTI_CUDA(cudaMalloc(&ds->err_dev, sizeof(uint32_t) * 4));
     FTI_CUDA(cudaMemset(ds->err_dev, 0, sizeof(uint32_t) * 4));
-    FTI_CUDA(cudaMalloc(&ds->prof_units, sizeof(unsigned long long) * FT_NUM_STAGES));
-    FTI_CUDA(cudaMemset(ds->prof_units, 0, sizeof(unsigned long long) * FT_NUM_STAGES));
+    FTI_CUDA(cudaMalloc(&ds->prof_units, sizeof(unsigned long long) * (FT_NUM_STAGES + 1)));
+    FTI_CUDA(cudaMemset(ds->prof_units, 0, sizeof(unsigned long long) * (FT_NUM_STAGES + 1)));
     *out = ds;
     return FT_OK;
 }

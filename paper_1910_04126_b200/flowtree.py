@@ -31,6 +31,7 @@ EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft
             "ft_profile_stage_name", "ft_launch_count", "ft_topk", "ft_flowtree_estimate_lists",
             "ft_exact_w1_lists"]
 FT_NUM_STAGES = 7
+FT_PROF_DIST_FLOPS = FT_NUM_STAGES   # ft_profile_units slot: distance-table algorithmic flops
 
 
 class FlowtreeError(RuntimeError):
