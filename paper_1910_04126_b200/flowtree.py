@@ -263,7 +263,7 @@ def ft_topk(vals, k: int, ids=None, id_base: int = 0, out_ids=None, out_val=None
 
 def ft_flowtree_estimate_lists(ds, q_off, q_ids, q_w, docs, out=None, stream=None):
     """Flowtree estimates of per-query candidate lists: docs is a DEVICE int64 [nq, n] tensor of doc
-    indices (negative = skipped, NaN out); returns a DEVICE float64 [nq, n] tensor."""
+    indices (negative = skipped, +inf out; >= n: NaN and FT_ERANGE); returns a DEVICE float64 [nq, n] tensor."""
     import torch
     q_off = np.ascontiguousarray(q_off, dtype=np.int64)
     nq = len(q_off) - 1

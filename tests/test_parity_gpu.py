@@ -263,6 +263,54 @@ def test_lane_per_pair_flowtree_matches_other_kernels(ft, monkeypatch, name, nq,
         np.testing.assert_allclose(a, c, rtol=1e-6, atol=0)
 
 
+@pytest.mark.parametrize("big", [False, True])
+def test_flowtree_degenerate_and_maximum_supports(ft, big):
+    """Supports at the edges of the lane-per-pair kernel's geometry, through the distance table
+    (d = 300): one-point and two-point docs and queries, shared and disjoint ids, non-uniform
+    weights; with big=True a 300-point doc and a 256-point query (beyond the kernel's 255-item
+    limit, so the warp kernel scores every pair).  All pairs against the oracle, and as candidate
+    lists with padding (-1 -> +inf) through the same path."""
+    import dataclasses
+    base = get_workload("reviews", n_docs=200, n_queries=2)
+    rng = np.random.default_rng(17)
+    N = base.X.shape[0]
+    sizes = [1, 1, 2, 2, 3, 17, 64, 90, 200, 255] + ([300] if big else [])
+    docs = [np.sort(rng.choice(N, s_, replace=False)).astype(np.int32) for s_ in sizes]
+    docs.append(docs[0].copy())                          # a duplicate one-point doc
+    docs.append(np.sort(np.concatenate([docs[2], docs[0]])).astype(np.int32))   # shares ids
+    dw = [rng.integers(1, 200, len(d_)).astype(np.uint32) for d_ in docs]
+    qs = [docs[0].copy(), docs[2].copy(), np.sort(rng.choice(N, 2, replace=False)).astype(np.int32),
+          np.sort(np.unique(np.concatenate([docs[6][:30], rng.choice(N, 60, replace=False)]))).astype(np.int32)]
+    if big:
+        qs.append(np.sort(rng.choice(N, 256, replace=False)).astype(np.int32))
+    qw = [rng.integers(1, 200, len(q_)).astype(np.uint32) for q_ in qs]
+    qw[1] = dw[2].copy()                                 # query 1 == doc 2 exactly: FT 0
+    wl = dataclasses.replace(
+        base, doc_off=np.concatenate([[0], np.cumsum([len(d_) for d_ in docs])]).astype(np.int64),
+        ids=np.concatenate(docs), w=np.concatenate(dw),
+        q_off=np.concatenate([[0], np.cumsum([len(q_) for q_ in qs])]).astype(np.int64),
+        q_ids=np.concatenate(qs), q_w=np.concatenate(qw))
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    got = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    pairs = [(q, d_) for q in range(wl.nq) for d_ in range(wl.n)]
+    ref = _oracle_all(T, wl, "ft", pairs)
+    assert_ft_close([got[q, d_] for q, d_ in pairs], ref, f"degenerate supports big={big}")
+    assert got[1, 2] == 0.0
+    import torch
+    dev = torch.device("cuda:0")
+    cand = np.tile(np.concatenate([np.arange(wl.n), [-1, -1, 3]]), (wl.nq, 1)).astype(np.int64)
+    out = torch.empty(cand.shape, dtype=torch.float64, device=dev)
+    ft.ft_flowtree_estimate_lists(ds.h, wl.q_off, torch.from_numpy(wl.q_ids).to(dev),
+                                  torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32),
+                                  torch.from_numpy(cand).to(dev), out)
+    ds.synchronize(torch.cuda.current_stream())
+    o = out.cpu().numpy()
+    assert np.all(np.isinf(o[:, wl.n:wl.n + 2]))
+    np.testing.assert_allclose(o[:, :wl.n], got, rtol=1e-6, atol=0)
+    np.testing.assert_array_equal(o[:, wl.n + 2], got[:, 3])
+
+
 @pytest.mark.parametrize("max_depth", [1, 2])
 def test_lane_per_pair_flowtree_capped_tree(ft, monkeypatch, max_depth):
     """A depth cap that binds (d = 300 mixture, D = 1 or 2) puts many points into multi-point
