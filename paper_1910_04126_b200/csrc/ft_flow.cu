@@ -93,6 +93,11 @@ __device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_
     // on the fly, FP32 direct differences (the query row from shared memory when staged)
     const float* xr = a.X + (int64_t)x * a.d;
     const float* yr = c.Y ? c.Y + jq * a.d : a.X + (int64_t)y * a.d;
+    if (a.d == 2) {   // planar ground sets (the image grid): the same FP32 operations, unrolled
+        const float2 xv = *(const float2*)xr;
+        const float d0 = xv.x - yr[0], d1 = xv.y - yr[1];
+        return sqrtf(fmaf(d1, d1, fmaf(d0, d0, 0.f)));
+    }
     float acc = 0.f;
     for (int t = 0; t < a.d; t++) {
         float df = xr[t] - yr[t];
@@ -129,6 +134,7 @@ __device__ void nw_corner(const PairCtx& c, const uint16_t* a_list, int la, cons
         carry = __shfl_sync(0xffffffffu, incl, 31);
     }
     const uint32_t TA = carry;
+    if (TA == 0) return;   // no doc mass left under the node: nothing matches, residuals unchanged
     carry = 0;
     for (int p0 = 0; p0 < lb; p0 += 32) {
         int p = p0 + lane;
