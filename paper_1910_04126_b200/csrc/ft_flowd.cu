@@ -1,9 +1,9 @@
 // ft_flowd.cu — a6 with LANE = PAIR: the Flowtree estimate (§3; greedy flow
 // PAPER.md:495-504) of 32 (query, doc) pairs per warp that share the query.
 //
-// A CTA works for one query: its items, its vocab bitmap + per-word rank (query item index of an
-// id) and, for a compact candidate table, its row map ({bits, rank} per 32 vocab ids) sit in
-// shared memory.  Lane l of a warp scores the pair (q, docs[base + l]) on its own:
+// A CTA works for one query: its items and its vocab bitmap + per-word rank (query item index of
+// an id) sit in shared memory; a compact candidate table's row map ({bits, rank} per 32 vocab ids)
+// is read through L2 (staging it cost a CTA per SM: 0.99 vs 0.86 ms per reviews k-NN batch).  Lane l of a warp scores the pair (q, docs[base + l]) on its own:
 //   * M-nodes: a cell with ≥ 2 ground points present on both sides where both keep residual mass
 //     after the leaves' self matches (so phase B of the warp kernel would match there) hands the
 //     pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
@@ -33,6 +33,9 @@ namespace {
 #endif
 constexpr int DW = 8;      // warps per CTA
 constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
+#ifndef FTD_GMAP
+#define FTD_GMAP 1         // 1: the compact table's row map is read from L2, not staged in shared memory
+#endif
 #ifndef FTD_DRB
 #define FTD_DRB 8
 #endif
@@ -71,10 +74,10 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const int q = a.q0 + (int)blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
     const QHeader* hdr = (const QHeader*)slot;
-    // shared: qitem[Sq] uint2 | smap[nw] uint2 (compact table) | qbits[nw] | qrank[nw] | queue[DW][DCAP][32]
+    // shared: qitem[Sq] uint2 | smap[nw] uint2 (compact table, FTD_GMAP=0 only) | qbits[nw] | qrank[nw] | queue[DW][DCAP][32]
     uint2* qitem = (uint2*)sm;
     uint2* smap = qitem + a.Sq;
-    uint32_t* qbits = (uint32_t*)(smap + (a.map ? a.nw : 0));
+    uint32_t* qbits = (uint32_t*)(smap + (a.map && !FTD_GMAP ? a.nw : 0));
     uint32_t* qrank = qbits + a.nw;
     uint16_t* queue = (uint16_t*)(qrank + a.nw);
     const uint32_t sq = hdr->s, U = hdr->U, mh_mask = hdr->mh_mask;
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const uint2* gitems = (const uint2*)(slot + a.L.off_items);
     for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) qitem[i] = gitems[i];
     for (int i = threadIdx.x; i < a.nw; i += blockDim.x) qbits[i] = 0u;
-    if (a.map) {
+    if (a.map && !FTD_GMAP) {
         const uint2* gm = a.map + (int64_t)q * a.nw;
         for (int i = threadIdx.x; i < a.nw; i += blockDim.x) smap[i] = gm[i];
     }
@@ -111,6 +114,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const float* trow = a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
     const uint32_t ld = (uint32_t)a.ld;
     const bool smap_on = a.map != nullptr;
+    const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
+    (void)gmapq;
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
     const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
     const bool qmn = hdr->n_mn > 0;
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
             ed = hit ? (cd < nc ? ne : DQ_END) : ed;
             uint32_t row = x;
             if (smap_on) {
-                const uint2 mw = smap[x >> 5];
+                const uint2 mw = FTD_GMAP ? __ldg(gmapq + (x >> 5)) : smap[x >> 5];
                 row = mw.y + __popc(mw.x & ((1u << (x & 31)) - 1u));
             }
             r_ = m - adj;
@@ -362,7 +367,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     DArgs a{};
     a.nw = (int)((ix->N + 31) / 32);
     a.Sq = std::max(1, L.smax);
-    const size_t smem = 8ull * a.Sq + (tab.map ? 8ull * a.nw : 0) + 8ull * a.nw + 2ull * DW * DCAP * 32;
+    const size_t smem = 8ull * a.Sq + (tab.map && !FTD_GMAP ? 8ull * a.nw : 0) + 8ull * a.nw + 2ull * DW * DCAP * 32;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     cudaError_t e;
     if ((e = ds->s_fblist.reserve((size_t)nq * n_docs * 4)) != cudaSuccess) return e;
@@ -387,7 +392,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     // the L1 caches the lanes' doc records between the pre-pass and the merge: give shared memory
     // only what the target CTAs per SM need (3, or 2 with the 25 KB-class candidate row map)
     {
-        const int ctas = tab.map ? 2 : FTD_MINB;
+        const int ctas = tab.map && !FTD_GMAP ? 2 : FTD_MINB;
         const size_t need = (size_t)ctas * (smem + 2176 + 1024);
         int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
         if (const char* ev = getenv("FT_FTD_CARVEOUT")) pct = atoi(ev);
