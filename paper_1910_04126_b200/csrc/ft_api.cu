@@ -224,6 +224,7 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         FTI_RES(ds->s_rows, (size_t)nq * rows_cap * 4);
         FTI_RES(ds->s_rowcnt, (size_t)nq * 4);
         FTI_RES(ds->s_rowbase, (size_t)qch * 8);
+        FTI_RES(ds->s_pitch, (size_t)qch * 4);
         StageTimer tm(ds, FTI_ST_VMAP, st);
         FTI_CUDA(fti_launch_vocab_map(ds, nq, d_docs, docs_ld, n_docs, ds->s_map.as<uint2>(), ds->s_rows.as<int32_t>(),
                                       ds->s_rowcnt.as<int32_t>(), rows_cap, st));
@@ -240,15 +241,18 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         tab.ld = ld;
         if (use_map) {
             StageTimer tm(ds, FTI_ST_VMAP, st);
-            FTI_CUDA(fti_launch_row_base(rowcnt_c, nqc, ds->s_rowbase.as<int64_t>(), st));
+            FTI_CUDA(fti_launch_row_base(rowcnt_c, qb, S.L, nqc, ds->s_rowbase.as<int64_t>(), ds->s_pitch.as<int32_t>(),
+                                         st));
             tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
             tab.row_base = ds->s_rowbase.as<int64_t>();
+            tab.pitch = ds->s_pitch.as<int32_t>();
         }
         {
             StageTimer tm(ds, FTI_ST_DIST, st);
             FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, rows_c, rowcnt_c, rows_cap,
                                            use_map ? ds->s_rowbase.as<int64_t>() : nullptr,
-                                           ds->s_table.as<float>(), ld, st));
+                                           use_map ? ds->s_pitch.as<int32_t>() : nullptr, ds->s_table.as<float>(), ld,
+                                           st));
         }
         StageTimer tm(ds, FTI_ST_FT, st);
         FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,

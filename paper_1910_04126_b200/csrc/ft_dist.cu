@@ -152,6 +152,7 @@ struct DistArgs {
     const int32_t* rowcnt;      // [nq] or null (rows_cap)
     int64_t rows_cap;
     const int64_t* row_base;    // [nq] or null (q * rows_cap)
+    const int32_t* pitch;       // [nq] per-query row pitch with row_base as an ELEMENT offset, or null
     float* table;
     int ld;
     int cb;                     // column block (query points cb*256 ...)
@@ -374,7 +375,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
         const int et = t - (NLOAD + 32);              // 0..32*NEPI-1 within the epilogue warps
         float* tbuf = tstage + (size_t)ew * 32 * TPITCH;   // this warp's 32x16 transpose buffer
         int k = 0, cur_q = -1, nb = 0;
-        int64_t rb = 0;
+        int64_t rb = 0;               // the query's table base (elements)
+        int32_t rld = a.ld;           // its row pitch
         // next tile's descriptor, row id and row norm, loaded one tile ahead
         int4 ndsc = make_int4(0, 0, 0, 0);
         float nnx = 0.f;
@@ -399,7 +401,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                 const QHeader* hdr = (const QHeader*)slot;
                 const int sq = hdr->err ? 0 : (int)hdr->s;
                 nb = min(NCB, max(0, sq - a.cb * NCB));
-                rb = a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap;
+                if (a.pitch) {
+                    rld = a.pitch[q];
+                    rb = a.row_base[q];                 // elements
+                } else {
+                    rld = a.ld;
+                    rb = (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
+                }
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
                 const uint2* qitems = (const uint2*)(slot + a.L.off_items);
                 for (int j = et; j < NCB; j += 32 * NEPI) {
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                 cur_q = q;
             }
             // rows of this warp: tile row 32*quarter + i; the table rows are contiguous
-            float* wrow0 = a.table + (rb + (int64_t)dsc.y * TM + quarter * 32) * a.ld + a.cb * NCB;
+            float* wrow0 = a.table + rb + ((int64_t)dsc.y * TM + quarter * 32) * rld + a.cb * NCB;
             const unsigned valid = __ballot_sync(0xffffffffu, xid >= 0);     // rows that exist (a prefix)
             TW(0, mbar_wait(&accf[b], (k >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                     }
                 }
                 if (DBG) dbg[2] += (unsigned long long)(clock64() - tc0);
-                if (c0 + 16 <= nb && (a.ld & 3) == 0) {
+                if (c0 + 16 <= nb && (rld & 3) == 0) {
                     // transpose through shared memory: lane (8 rows x 4 granules per store) writes 16 B of
                     // a row, so each store instruction covers 8 rows x 64 contiguous bytes
 #pragma unroll
@@ -458,14 +466,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                     for (int s8 = 0; s8 < 4; s8++) {
                         const int row = 8 * s8 + ra;
                         if ((valid >> row) & 1u)
-                            *(float4*)(wrow0 + (int64_t)row * a.ld + c0 + 4 * gb) =
+                            *(float4*)(wrow0 + (int64_t)row * rld + c0 + 4 * gb) =
                                 *(const float4*)(tbuf + row * TPITCH + 4 * gb);
                     }
                     __syncwarp();
                 } else if (xid >= 0) {
 #pragma unroll
                     for (int i = 0; i < 16; i++)
-                        if (c0 + i < nb) wrow0[(int64_t)lane * a.ld + c0 + i] = o[i];
+                        if (c0 + i < nb) wrow0[(int64_t)lane * rld + c0 + i] = o[i];
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -659,13 +667,29 @@ __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc
 }
 
 // compact table placement: exclusive prefix of the per-query row counts
-__global__ void k_row_base(const int32_t* __restrict__ rowcnt, int nq, int64_t* __restrict__ row_base) {
-    if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        for (int q = 0; q < nq; q++) {
-            row_base[q] = acc;
-            acc += rowcnt[q];
+// compact tables: query q's rows start at ELEMENT row_base[q], pitch[q] = its support rounded up to
+// 8 floats (32-byte rows), so a table is rows_q · pitch_q floats rather than rows_q · (batch max)
+// (one CTA, block-wide scans over 1024-query slabs; a table of rows_q · pitch_q < 2^31 floats)
+__global__ void __launch_bounds__(1024) k_row_base(const int32_t* __restrict__ rowcnt,
+                                                   const uint8_t* __restrict__ qblock, QueryLayout L, int nq,
+                                                   int64_t* __restrict__ row_base, int32_t* __restrict__ pitch) {
+    __shared__ int tmp[32];
+    int64_t acc = 0;
+    for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        int32_t p = 8, sz = 0;
+        if (q < nq) {
+            const QHeader* h = (const QHeader*)(qblock + (size_t)q * L.stride);
+            p = ((int32_t)(h->err ? 1u : (h->s > 0 ? h->s : 1u)) + 7) & ~7;
+            sz = rowcnt[q] * p;
         }
+        int tot;
+        const int ex = fti_block_exclusive_sum(sz, tmp, &tot);
+        if (q < nq) {
+            row_base[q] = acc + ex;
+            pitch[q] = p;
+        }
+        acc += tot;
     }
 }
 
@@ -697,7 +721,8 @@ cudaError_t prepare_centered(ft_index* ix, cudaStream_t st) {
 
 cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
-                                  const int64_t* d_row_base, float* d_table, int32_t ld, cudaStream_t st) {
+                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, int32_t ld,
+                                  cudaStream_t st) {
     if (nq <= 0 || rows_cap <= 0) return cudaSuccess;
     ft_index* ix = const_cast<ft_index*>(ds->ix);
     cudaError_t e;
@@ -715,6 +740,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.rowcnt = d_rowcnt;
     a.rows_cap = rows_cap;
     a.row_base = d_row_base;
+    a.pitch = d_pitch;
     a.table = d_table;
     a.ld = ld;
     const int ncb = (L.smax + NCB - 1) / NCB;
@@ -786,9 +812,10 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
     return cudaGetLastError();
 }
 
-cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, int32_t nq, int64_t* d_row_base, cudaStream_t st) {
+cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, const uint8_t* d_qblock, const QueryLayout& L, int32_t nq,
+                                int64_t* d_row_base, int32_t* d_pitch, cudaStream_t st) {
     if (nq <= 0) return cudaSuccess;
-    k_row_base<<<1, 32, 0, st>>>(d_rowcnt, nq, d_row_base);
+    k_row_base<<<1, 1024, 0, st>>>(d_rowcnt, d_qblock, L, nq, d_row_base, d_pitch);
     fti_count_launches(1);
     return cudaGetLastError();
 }

@@ -77,6 +77,7 @@ struct PairCtx {
     uint32_t* qres;
     uint32_t* qcum;
     const float* trow_base; // table for this query or null
+    uint32_t tld;           // its row pitch
     const uint2* map;       // candidate-vocabulary bitmap {bits, rank} per 32 ids, or null (row = vocab)
 };
 
@@ -88,7 +89,7 @@ __device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_
             const uint2 m = c.map[x >> 5];
             row = (int64_t)(m.y + __popc(m.x & ((1u << (x & 31)) - 1u)));
         }
-        return c.trow_base[row * a.tab.ld + jq];
+        return c.trow_base[row * c.tld + jq];
     }
     // on the fly, FP32 direct differences (the query row from shared memory when staged)
     const float* xr = a.X + (int64_t)x * a.d;
@@ -268,7 +269,7 @@ __device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& c
                 }
                 float dv[RB];
 #pragma unroll
-                for (int u = 0; u < RB; u++) dv[u] = ex[u] ? c.trow_base[(int64_t)rv[u] * fa.tab.ld + jv[u]] : 0.f;
+                for (int u = 0; u < RB; u++) dv[u] = ex[u] ? c.trow_base[(int64_t)rv[u] * c.tld + jv[u]] : 0.f;
 #pragma unroll
                 for (int u = 0; u < RB; u++)
                     if (ex[u]) acc = fmaf((float)ex[u], dv[u], acc);
@@ -358,9 +359,15 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     c.dcum = wsm + 2 * a.Sd;
     c.qres = wsm + 3 * a.Sd;
     c.qcum = wsm + 3 * a.Sd + a.Sq;
-    c.trow_base = a.tab.table ? a.tab.table + (a.tab.row_base ? a.tab.row_base[q] : (int64_t)q * a.tab.rows_cap) *
-                                                  a.tab.ld
-                              : nullptr;
+    if (a.tab.table && a.tab.pitch) {
+        c.trow_base = a.tab.table + a.tab.row_base[q];
+        c.tld = (uint32_t)a.tab.pitch[q];
+    } else {
+        c.trow_base = a.tab.table ? a.tab.table + (a.tab.row_base ? a.tab.row_base[q] : (int64_t)q * a.tab.rows_cap) *
+                                                      a.tab.ld
+                                  : nullptr;
+        c.tld = (uint32_t)a.tab.ld;
+    }
     c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
 
     unsigned long long ubytes = 0;

@@ -57,6 +57,7 @@ struct DArgs {
     const float* table;
     const uint2* map;          // [nq][nw] {bits, rank} rows of the compact table, or null (row = vocab id)
     const int64_t* row_base;   // [nq] or null (q * rows_cap)
+    const int32_t* pitch;      // [nq] per-query pitch (row_base in elements), or null
     int64_t rows_cap;
     int32_t ld;
     int32_t nw, Sq;
@@ -111,8 +112,9 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint16_t* myq = queue + warp * DCAP * 32 + lane;
-    const float* trow = a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
-    const uint32_t ld = (uint32_t)a.ld;
+    const float* trow = a.pitch ? a.table + a.row_base[q]
+                                : a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
+    const uint32_t ld = (uint32_t)(a.pitch ? a.pitch[q] : a.ld);
     const bool smap_on = a.map != nullptr;
     const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
     (void)gmapq;
@@ -377,7 +379,8 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.mn_off = ds->mn_off; a.mnodes = ds->mnodes; a.mlists = ds->mlists;
     a.qblock = d_qblock; a.L = L;
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;
-    a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.rows_cap = tab.rows_cap; a.ld = tab.ld;
+    a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.pitch = tab.pitch; a.rows_cap = tab.rows_cap;
+    a.ld = tab.ld;
     a.out = d_out; a.out_ld = out_ld;
     a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;
     a.err = ds->err_dev;

@@ -153,7 +153,7 @@ struct ft_dataset {
     unsigned long long* prof_units = nullptr;   // device [FT_NUM_STAGES] algorithmic bytes per stage
     unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
-    DevBuf s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
+    DevBuf s_pitch, s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
     DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_ftxchunk;
 };
 
@@ -173,6 +173,7 @@ struct FtTable {
     const float* table = nullptr;      // rows of ld floats, or null (on-the-fly distances)
     const uint2* map = nullptr;        // [nq][ceil(N/32)] {bits, rank}: row = rank + popc(bits below), or null
     const int64_t* row_base = nullptr; // [nq] first row of each query (compact), or null (q * rows_cap)
+    const int32_t* pitch = nullptr;    // [nq] per-query row pitch; then row_base is an ELEMENT offset
     int64_t rows_cap = 0;
     int32_t ld = 0;
 };
@@ -197,11 +198,13 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           cudaStream_t st);
 cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
-                                  const int64_t* d_row_base, float* d_table, int32_t ld, cudaStream_t st);
+                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, int32_t ld,
+                                  cudaStream_t st);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  cudaStream_t st);
-cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, int32_t nq, int64_t* d_row_base, cudaStream_t st);
+cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, const uint8_t* d_qblock, const QueryLayout& L, int32_t nq,
+                                int64_t* d_row_base, int32_t* d_pitch, cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
                               int* d_scratch /* rows + 1 ints */, cudaStream_t st, int64_t id_base = 0);
