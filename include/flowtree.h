@@ -168,6 +168,39 @@ ft_status ft_profile_units(ft_dataset* ds, int32_t stage, uint64_t* bytes);
 const char* ft_profile_stage_name(int32_t stage);
 uint64_t ft_launch_count(void);
 
+/* Process-wide tuning and test options (not part of the method; the defaults are the product
+ * configuration).  Each is read by the library on every call that uses it; nothing is read from
+ * the environment.  FT_EINVAL for an unknown option or a value out of range.
+ *   FT_OPT_VOCAB_HASH      1: the warp Flowtree kernel looks vocab ids up in the query's hash
+ *                          instead of the shared-memory bitmap (the path taken when N > 2^19).
+ *   FT_OPT_WARP_ONLY       1: every Flowtree pair runs on the warp kernel (k_flowtree), not the
+ *                          lane-per-pair kernel (k_ftd).
+ *   FT_OPT_QT_HASH         1: the Quadtree scan uses the hash chunk structure, not the dense one.
+ *   FT_OPT_SELECT_RADIX    1: selection uses the radix kernel for every row.
+ *   FT_OPT_EXACT_START_NW  1: the exact-W1 simplex starts from the northwest corner.
+ *   FT_OPT_TABLE_CHUNK     > 0: at most this many queries per distance-table chunk.
+ *   FT_OPT_TABLE_BUDGET_MB > 0: distance-table bytes per chunk (default: 1/4 of free HBM at the
+ *                          dataset's first Flowtree call, at most 48 GB).
+ *   FT_OPT_QT_WAVES        > 0: CTA waves per SM slot of the Quadtree launch (default 8).
+ *   FT_OPT_FTD_CARVEOUT    1..100: k_ftd shared-memory carveout percent (0: sized for 3 CTAs/SM).
+ *   FT_OPT_DEBUG           bit mask of diagnostics printed to stderr: 1 distance-table role
+ *                          clocks, 2 exact-W1 pivots, 4 selection paths, 8 scratch growth.       */
+typedef enum {
+    FT_OPT_VOCAB_HASH = 0,
+    FT_OPT_WARP_ONLY = 1,
+    FT_OPT_QT_HASH = 2,
+    FT_OPT_SELECT_RADIX = 3,
+    FT_OPT_EXACT_START_NW = 4,
+    FT_OPT_TABLE_CHUNK = 5,
+    FT_OPT_TABLE_BUDGET_MB = 6,
+    FT_OPT_QT_WAVES = 7,
+    FT_OPT_FTD_CARVEOUT = 8,
+    FT_OPT_DEBUG = 9,
+    FT_NUM_OPTIONS = 10
+} ft_option;
+ft_status ft_set_option(int32_t option, int64_t value);
+ft_status ft_get_option(int32_t option, int64_t* value);
+
 void ft_index_free(ft_index* ix);
 void ft_dataset_free(ft_dataset* ds);
 /* Thread-local message of the last failing call on this thread ("" if none).                 */

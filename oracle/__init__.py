@@ -44,15 +44,24 @@ class OracleError(RuntimeError):
         self.code = code
 
 
-def build_oracle(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain -O2, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+# ORACLE_SANITIZE=1 (tests/test_oracle_sanitizers.py): load an AddressSanitizer + UBSan build
+_SAN = os.environ.get("ORACLE_SANITIZE") == "1"
+_SAN_LIB_PATH = os.path.join(_HERE, "liboracle_san.so")
+
+
+def build_oracle(force: bool = False, sanitize: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, no FMA contraction, no fast-math); with
+    ``sanitize`` an -fsanitize=address,undefined build (abort on the first report)."""
+    path = _SAN_LIB_PATH if sanitize else _LIB_PATH
+    if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+        tmp = path + f".tmp{os.getpid()}"
+        extra = ["-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+                 "-fno-omit-frame-pointer"] if sanitize else []
         subprocess.check_call([
-            "gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+            "gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-Wall"] + extra + [
             "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB_PATH)
-    return _LIB_PATH
+        os.replace(tmp, path)
+    return path
 
 
 def _load():
@@ -60,7 +69,7 @@ def _load():
     with _lock:
         if _lib is not None:
             return _lib
-        lib = ctypes.CDLL(build_oracle())
+        lib = ctypes.CDLL(build_oracle(sanitize=_SAN))
         P = ctypes.c_void_p
         i32, i64, u64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
         lib.or_splitmix64.restype = u64

@@ -24,6 +24,24 @@ void fti_count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_o
 extern "C" const char* ft_last_error(void) { return g_last_error.c_str(); }
 extern "C" uint64_t ft_launch_count(void) { return g_launches.load(); }
 
+static std::atomic<int64_t> g_opts[FT_NUM_OPTIONS];
+
+int64_t fti_opt(int option) { return g_opts[option].load(std::memory_order_relaxed); }
+
+extern "C" ft_status ft_set_option(int32_t option, int64_t value) {
+    if (option < 0 || option >= FT_NUM_OPTIONS) return fti_fail(FT_EINVAL, "ft_set_option: unknown option");
+    if (value < 0) return fti_fail(FT_EINVAL, "ft_set_option: negative value");
+    if (option == FT_OPT_FTD_CARVEOUT && value > 100) return fti_fail(FT_EINVAL, "ft_set_option: carveout > 100");
+    g_opts[option].store(value, std::memory_order_relaxed);
+    return FT_OK;
+}
+
+extern "C" ft_status ft_get_option(int32_t option, int64_t* value) {
+    if (option < 0 || option >= FT_NUM_OPTIONS || !value) return fti_fail(FT_EINVAL, "ft_get_option: bad argument");
+    *value = g_opts[option].load(std::memory_order_relaxed);
+    return FT_OK;
+}
+
 namespace {
 
 // records a CUDA event pair around one stage when profiling is enabled on the dataset
@@ -72,6 +90,16 @@ bool is_device_ptr(const void* p) {
                                                               cudaGetErrorString(_e));          \
     } while (0)
 
+// a Flowtree launch; cudaErrorInvalidConfiguration means the supports do not fit the kernels'
+// shared-memory geometry (a size limit, FT_ERANGE)
+#define FTI_FT(call)                                                                                       \
+    do {                                                                                                   \
+        cudaError_t _e = (call);                                                                           \
+        if (_e == cudaErrorInvalidConfiguration)                                                           \
+            return fti_fail(FT_ERANGE, "Flowtree: doc/query supports too large for the kernel geometry");  \
+        if (_e != cudaSuccess) return fti_fail(FT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
 // device error word (sticky) -> status
 ft_status check_device_errors(const ft_dataset* ds, cudaStream_t st, const char* who) {
     uint32_t h = 0;
@@ -91,6 +119,7 @@ struct Staged {
     const int32_t* qids = nullptr;
     const uint32_t* qw = nullptr;
     const int64_t* qoff_dev = nullptr;
+    const int64_t* qoff_host = nullptr;
     uint8_t* qblock = nullptr;
 };
 
@@ -137,6 +166,7 @@ ft_status stage_queries(ft_dataset* ds, const int64_t* q_off, int32_t nq, const 
         }
     }
     S.L = fti_query_layout(ix, smax);
+    S.qoff_host = q_off;
     FTI_RES(ds->s_qoff, sizeof(int64_t) * (nq + 1));
     FTI_CUDA(cudaMemcpyAsync(ds->s_qoff.p, q_off, sizeof(int64_t) * (nq + 1), cudaMemcpyHostToDevice, st));
     S.qoff_dev = ds->s_qoff.as<int64_t>();
@@ -189,23 +219,12 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     const ft_index* ix = ds->ix;
     if (ix->d <= FTI_SMALL_D) {
         StageTimer tm(ds, FTI_ST_FT, st);
-        FTI_CUDA(fti_launch_ft(ds, S.L, S.qblock, nq, d_docs, docs_ld, n_docs, FtTable{}, d_out, out_ld, nullptr,
-                               nullptr, 0, st));
+        FTI_FT(fti_launch_ft(ds, S.L, S.qblock, nq, d_docs, docs_ld, n_docs, FtTable{}, d_out, out_ld, nullptr,
+                             nullptr, 0, st));
         return FT_OK;
     }
-    const int32_t ld = (S.L.smax + 3) & ~3;
-    const bool use_map = d_docs != nullptr;
-    const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
-    // query chunks bounded by the worst-case table allocation (tables are written compactly, so
-    // only the actual rows are touched).  Larger chunks keep the distance-table and Flowtree grids
-    // full (reviews: one chunk of 1,000 queries runs 10% faster than chunks of 90), so the budget
-    // is a quarter of the free HBM, at most 48 GB; FT_TABLE_BUDGET_GB / FT_TABLE_CHUNK override
-    // (test hooks for the chunk boundaries).
-    const size_t nwords = (size_t)(ix->N + 31) / 32;
-    const size_t per_q = (size_t)rows_cap * ld * 4;
     // the budget is fixed at the dataset's first Flowtree call: cudaMemGetInfo on every call showed
-    // as occasional multi-ms host stalls (the query is not free), and a stable budget keeps the
-    // table allocation from changing size between calls
+    // as occasional multi-ms host stalls, and a stable budget keeps the allocation from changing
     if (ds->table_budget == 0) {
         size_t fr = 0, tot = 0;
         ds->table_budget = (size_t)3 << 30;
@@ -213,24 +232,52 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
             ds->table_budget = std::max(ds->table_budget, std::min(fr / 4, (size_t)48 << 30));
     }
     size_t budget = ds->table_budget;
-    if (const char* eb = getenv("FT_TABLE_BUDGET_GB")) budget = (size_t)atoi(eb) << 30;
-    int32_t qch = (int32_t)std::max<size_t>(1, std::min<size_t>((size_t)nq, budget / per_q));
-    if (const char* ev = getenv("FT_TABLE_CHUNK")) qch = std::max(1, std::min(qch, atoi(ev)));
-    FTI_RES(ds->s_table, (size_t)qch * rows_cap * ld * 4);
+    if (fti_opt(FT_OPT_TABLE_BUDGET_MB) > 0) budget = (size_t)fti_opt(FT_OPT_TABLE_BUDGET_MB) << 20;
+    const int64_t qcap = fti_opt(FT_OPT_TABLE_CHUNK) > 0 ? fti_opt(FT_OPT_TABLE_CHUNK) : (int64_t)nq;
+    // per query: table rows, pitch (floats) and ELEMENT offset within its chunk.  With candidate
+    // lists the rows are the candidates' vocabulary (compact, counted on the device by k_vocab and
+    // read back once: the tables are then sized exactly); exhaustively every vocab id is a row.
+    const bool use_map = d_docs != nullptr;
+    const int64_t rows_cap = use_map ? std::min<int64_t>(ix->N, n_docs * (int64_t)ds->max_s) : ix->N;
+    const size_t nwords = (size_t)(ix->N + 31) / 32;
+    std::vector<int32_t> rowcnt((size_t)nq, (int32_t)ix->N);
     if (use_map) {
-        // candidate vocabulary of every query in one launch (a CTA per query fills the GPU); the
-        // per-chunk table placement is a prefix over the chunk's row counts
         FTI_RES(ds->s_map, (size_t)nq * nwords * 8);
         FTI_RES(ds->s_rows, (size_t)nq * rows_cap * 4);
         FTI_RES(ds->s_rowcnt, (size_t)nq * 4);
-        FTI_RES(ds->s_rowbase, (size_t)qch * 8);
-        FTI_RES(ds->s_pitch, (size_t)qch * 4);
         StageTimer tm(ds, FTI_ST_VMAP, st);
         FTI_CUDA(fti_launch_vocab_map(ds, nq, d_docs, docs_ld, n_docs, ds->s_map.as<uint2>(), ds->s_rows.as<int32_t>(),
                                       ds->s_rowcnt.as<int32_t>(), rows_cap, st));
+        FTI_CUDA(cudaMemcpyAsync(rowcnt.data(), ds->s_rowcnt.p, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+        FTI_CUDA(cudaStreamSynchronize(st));
     }
-    for (int32_t q0 = 0; q0 < nq; q0 += qch) {
-        const int32_t nqc = std::min(qch, nq - q0);
+    std::vector<int64_t> base((size_t)nq);
+    std::vector<int32_t> pitch((size_t)nq);
+    std::vector<int32_t> chunk_q0;       // first query of each chunk
+    size_t chunk_max = 0, cur = 0;
+    int64_t in_chunk = 0;
+    for (int32_t q = 0; q < nq; q++) {
+        const int64_t s = S.qoff_host[q + 1] - S.qoff_host[q];
+        pitch[q] = (int32_t)((s + 7) & ~7);          // 32-byte rows
+        const size_t bytes = (size_t)rowcnt[q] * (size_t)pitch[q] * 4;
+        if (q == 0 || in_chunk >= qcap || (cur > 0 && cur + bytes > budget)) {
+            chunk_q0.push_back(q);
+            cur = 0;
+            in_chunk = 0;
+        }
+        base[q] = (int64_t)(cur / 4);
+        cur += bytes;
+        in_chunk++;
+        chunk_max = std::max(chunk_max, cur);
+    }
+    chunk_q0.push_back(nq);
+    FTI_RES(ds->s_table, std::max<size_t>(chunk_max, 4));
+    FTI_RES(ds->s_rowbase, (size_t)nq * 8);
+    FTI_RES(ds->s_pitch, (size_t)nq * 4);
+    FTI_CUDA(cudaMemcpyAsync(ds->s_rowbase.p, base.data(), (size_t)nq * 8, cudaMemcpyHostToDevice, st));
+    FTI_CUDA(cudaMemcpyAsync(ds->s_pitch.p, pitch.data(), (size_t)nq * 4, cudaMemcpyHostToDevice, st));
+    for (size_t c = 0; c + 1 < chunk_q0.size(); c++) {
+        const int32_t q0 = chunk_q0[c], nqc = chunk_q0[c + 1] - q0;
         const uint8_t* qb = S.qblock + (size_t)q0 * S.L.stride;
         const int64_t* dq = d_docs ? d_docs + (int64_t)q0 * docs_ld : nullptr;
         const int32_t* rows_c = use_map ? ds->s_rows.as<int32_t>() + (int64_t)q0 * rows_cap : nullptr;
@@ -238,25 +285,17 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         FtTable tab;
         tab.table = ds->s_table.as<float>();
         tab.rows_cap = rows_cap;
-        tab.ld = ld;
-        if (use_map) {
-            StageTimer tm(ds, FTI_ST_VMAP, st);
-            FTI_CUDA(fti_launch_row_base(rowcnt_c, qb, S.L, nqc, ds->s_rowbase.as<int64_t>(), ds->s_pitch.as<int32_t>(),
-                                         st));
-            tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
-            tab.row_base = ds->s_rowbase.as<int64_t>();
-            tab.pitch = ds->s_pitch.as<int32_t>();
-        }
+        tab.row_base = ds->s_rowbase.as<int64_t>() + q0;
+        tab.pitch = ds->s_pitch.as<int32_t>() + q0;
+        if (use_map) tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
         {
             StageTimer tm(ds, FTI_ST_DIST, st);
-            FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, rows_c, rowcnt_c, rows_cap,
-                                           use_map ? ds->s_rowbase.as<int64_t>() : nullptr,
-                                           use_map ? ds->s_pitch.as<int32_t>() : nullptr, ds->s_table.as<float>(), ld,
-                                           st));
+            FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, rows_c, rowcnt_c, rows_cap, tab.row_base, tab.pitch,
+                                           ds->s_table.as<float>(), st));
         }
         StageTimer tm(ds, FTI_ST_FT, st);
-        FTI_CUDA(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,
-                               nullptr, nullptr, 0, st));
+        FTI_FT(fti_launch_ft(ds, S.L, qb, nqc, dq, docs_ld, n_docs, tab, d_out + (int64_t)q0 * out_ld, out_ld,
+                             nullptr, nullptr, 0, st));
     }
     return FT_OK;
 }
@@ -330,8 +369,8 @@ extern "C" ft_status ft_flowtree_flow(const ft_dataset* cds, int32_t q_len, cons
     FTI_RES(ds->s_flowcnt, sizeof(uint32_t));
     FTI_CUDA(cudaMemsetAsync(ds->s_flowcnt.p, 0, sizeof(uint32_t), st));
     FTI_RES(ds->s_vals, sizeof(double));
-    FTI_CUDA(fti_launch_ft(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{}, ds->s_vals.as<double>(), 1,
-                           ds->s_flow.as<uint32_t>(), ds->s_flowcnt.as<uint32_t>(), fcap, st));
+    FTI_FT(fti_launch_ft(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{}, ds->s_vals.as<double>(), 1,
+                         ds->s_flow.as<uint32_t>(), ds->s_flowcnt.as<uint32_t>(), fcap, st));
     uint32_t cnt = 0;
     FTI_CUDA(cudaMemcpyAsync(&cnt, ds->s_flowcnt.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     rc = check_device_errors(ds, st, who);
@@ -441,11 +480,14 @@ extern "C" ft_status ft_topk(const double* vals, int64_t vals_ld, const int64_t*
         return fti_fail(FT_EINVAL, "ft_topk: device pointers required");
     if (vals_ld < L || (ids && ids_ld < L)) return fti_fail(FT_EINVAL, "ft_topk: leading dimension < L");
     cudaStream_t st = (cudaStream_t)stream;
-    static DevBuf scratch;
-    FTI_CUDA(scratch.reserve(sizeof(int) * ((size_t)rows + 1)));
-    FTI_CUDA(fti_launch_select(vals, vals_ld, ids, ids_ld, L, rows, k, out_ids, out_val, k, scratch.as<int>(), st,
-                               id_base));
-    (void)who;
+    // the selection's scratch (redo counter + row list) is stream-ordered per call, so concurrent
+    // calls on different streams or devices never share it
+    int* scratch = nullptr;
+    FTI_CUDA(cudaMallocAsync((void**)&scratch, sizeof(int) * ((size_t)rows + 1), st));
+    const cudaError_t e = fti_launch_select(vals, vals_ld, ids, ids_ld, L, rows, k, out_ids, out_val, k, scratch, st,
+                                            id_base);
+    FTI_CUDA(cudaFreeAsync(scratch, st));
+    if (e != cudaSuccess) return fti_fail(FT_ECUDA, std::string(who) + ": " + cudaGetErrorString(e));
     return FT_OK;
 }
 

@@ -32,7 +32,7 @@
 //
 // Candidate vocabulary for the prefiltered pipeline: k_vocab marks every vocab id of the query's
 // m candidates in a shared-memory bitmap and turns it into dense row ids and the row list;
-// k_row_base places each query's rows compactly.
+// the host places each query's rows compactly (ft_api.cu).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -151,10 +151,9 @@ struct DistArgs {
     const int32_t* rows;        // [nq][rows_cap] or null (row = vocab)
     const int32_t* rowcnt;      // [nq] or null (rows_cap)
     int64_t rows_cap;
-    const int64_t* row_base;    // [nq] or null (q * rows_cap)
-    const int32_t* pitch;       // [nq] per-query row pitch with row_base as an ELEMENT offset, or null
+    const int64_t* row_base;    // [nq] ELEMENT offset of each query's table
+    const int32_t* pitch;       // [nq] per-query row pitch (floats)
     float* table;
-    int ld;
     int cb;                     // column block (query points cb*256 ...)
     int NPmax;                  // B stage capacity: max N_q of the launch
     int Q;                      // raw ring depth (chunks in flight)
@@ -376,7 +375,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
         float* tbuf = tstage + (size_t)ew * 32 * TPITCH;   // this warp's 32x16 transpose buffer
         int k = 0, cur_q = -1, nb = 0;
         int64_t rb = 0;               // the query's table base (elements)
-        int32_t rld = a.ld;           // its row pitch
+        int32_t rld = 8;              // its row pitch
         // next tile's descriptor, row id and row norm, loaded one tile ahead
         int4 ndsc = make_int4(0, 0, 0, 0);
         float nnx = 0.f;
@@ -401,13 +400,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_tc(DistArgs a) {
                 const QHeader* hdr = (const QHeader*)slot;
                 const int sq = hdr->err ? 0 : (int)hdr->s;
                 nb = min(NCB, max(0, sq - a.cb * NCB));
-                if (a.pitch) {
-                    rld = a.pitch[q];
-                    rb = a.row_base[q];                 // elements
-                } else {
-                    rld = a.ld;
-                    rb = (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
-                }
+                rld = a.pitch[q];
+                rb = a.row_base[q];                 // elements
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
                 const uint2* qitems = (const uint2*)(slot + a.L.off_items);
                 for (int j = et; j < NCB; j += 32 * NEPI) {
@@ -625,7 +619,7 @@ __global__ void __launch_bounds__(256) k_center_rows(const float* __restrict__ X
 // per-word ranks (dense row ids in vocab order), the row list and the row count
 __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc_off, const uint2* __restrict__ items,
                                                 const int64_t* __restrict__ cand, int64_t cand_ld, int64_t n_cand,
-                                                int64_t nwords, uint2* __restrict__ map, int32_t* __restrict__ rows,
+                                                int64_t n, int64_t nwords, uint2* __restrict__ map, int32_t* __restrict__ rows,
                                                 int32_t* __restrict__ rowcnt, int64_t rows_cap) {
     extern __shared__ uint32_t sbits[];
     __shared__ int tmp[32];
@@ -635,7 +629,9 @@ __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t c = warp; c < n_cand; c += nw) {
         const int64_t doc = cand[(int64_t)q * cand_ld + c];
-        if (doc < 0) continue;
+        // a negative candidate (padding / another shard's doc) has no rows; an index >= n is
+        // reported (NaN + FT_ERANGE) by the Flowtree kernels and contributes no rows here
+        if (doc < 0 || doc >= n) continue;
         const uint32_t i0 = doc_off[doc], i1 = doc_off[doc + 1];
         for (uint32_t i = i0 + lane; i < i1; i += 32) {
             const uint32_t x = items[i].x & FTI_VOCAB_MASK;
@@ -666,33 +662,6 @@ __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc
     if (threadIdx.x == 0) rowcnt[q] = run < rows_cap ? run : (int32_t)rows_cap;
 }
 
-// compact table placement: exclusive prefix of the per-query row counts
-// compact tables: query q's rows start at ELEMENT row_base[q], pitch[q] = its support rounded up to
-// 8 floats (32-byte rows), so a table is rows_q · pitch_q floats rather than rows_q · (batch max)
-// (one CTA, block-wide scans over 1024-query slabs; a table of rows_q · pitch_q < 2^31 floats)
-__global__ void __launch_bounds__(1024) k_row_base(const int32_t* __restrict__ rowcnt,
-                                                   const uint8_t* __restrict__ qblock, QueryLayout L, int nq,
-                                                   int64_t* __restrict__ row_base, int32_t* __restrict__ pitch) {
-    __shared__ int tmp[32];
-    int64_t acc = 0;
-    for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
-        const int q = q0 + threadIdx.x;
-        int32_t p = 8, sz = 0;
-        if (q < nq) {
-            const QHeader* h = (const QHeader*)(qblock + (size_t)q * L.stride);
-            p = ((int32_t)(h->err ? 1u : (h->s > 0 ? h->s : 1u)) + 7) & ~7;
-            sz = rowcnt[q] * p;
-        }
-        int tot;
-        const int ex = fti_block_exclusive_sum(sz, tmp, &tot);
-        if (q < nq) {
-            row_base[q] = acc + ex;
-            pitch[q] = p;
-        }
-        acc += tot;
-    }
-}
-
 // the index's translated operand, built once on first use
 cudaError_t prepare_centered(ft_index* ix, cudaStream_t st) {
     if (ix->Xc) return cudaSuccess;
@@ -721,8 +690,7 @@ cudaError_t prepare_centered(ft_index* ix, cudaStream_t st) {
 
 cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
-                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, int32_t ld,
-                                  cudaStream_t st) {
+                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, cudaStream_t st) {
     if (nq <= 0 || rows_cap <= 0) return cudaSuccess;
     ft_index* ix = const_cast<ft_index*>(ds->ix);
     cudaError_t e;
@@ -742,7 +710,6 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.row_base = d_row_base;
     a.pitch = d_pitch;
     a.table = d_table;
-    a.ld = ld;
     const int ncb = (L.smax + NCB - 1) / NCB;
     const int np_max = std::min(NCB, L.smax);
     a.NPmax = std::max(16, ((np_max + 15) / 16) * 16);
@@ -771,7 +738,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     if (Q < 2) return cudaErrorInvalidConfiguration;
     a.Q = Q;
     const size_t smem = (size_t)Q * raw_bytes + (size_t)MAXASLOT * b_slot + fixed;
-    const bool dbg = getenv("FT_DIST_DBG") != nullptr;
+    const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_DIST) != 0;
     auto kern = dbg ? k_dist_tc<true> : k_dist_tc<false>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
@@ -806,16 +773,8 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;   // N > 1.6M: not supported by the bitmap
     cudaError_t e = cudaFuncSetAttribute(k_vocab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_vocab<<<nq, 1024, smem, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, nwords, d_map, d_rows, d_rowcnt,
-                                    rows_cap);
-    fti_count_launches(1);
-    return cudaGetLastError();
-}
-
-cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, const uint8_t* d_qblock, const QueryLayout& L, int32_t nq,
-                                int64_t* d_row_base, int32_t* d_pitch, cudaStream_t st) {
-    if (nq <= 0) return cudaSuccess;
-    k_row_base<<<1, 1024, 0, st>>>(d_rowcnt, d_qblock, L, nq, d_row_base, d_pitch);
+    k_vocab<<<nq, 1024, smem, st>>>(ds->doc_off, ds->items, d_cand, cand_ld, n_cand, ds->n, nwords, d_map, d_rows,
+                                    d_rowcnt, rows_cap);
     fti_count_launches(1);
     return cudaGetLastError();
 }

@@ -586,8 +586,7 @@ cudaError_t fti_launch_exact(ft_dataset* ds, const QueryLayout& L, const uint8_t
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_per_q = n_per_q;
     a.out = d_out; a.out_ld = out_ld;
     a.err = ds->err_dev;
-    const char* gs = getenv("FT_EXACT_START");
-    a.greedy = !(gs && strcmp(gs, "nw") == 0);
+    a.greedy = fti_opt(FT_OPT_EXACT_START_NW) ? 0 : 1;
     // geometry from the largest supports (doc side from the dataset, query side from the batch);
     // pairs beyond EX_MAXV − 1 nodes or the shared-memory budget fail alone (NaN + FTI_ERR_CAP)
     const int Mx = std::max(1, (int)ds->max_s), Nx = std::max(1, (int)L.smax);
@@ -595,7 +594,7 @@ cudaError_t fti_launch_exact(ft_dataset* ds, const QueryLayout& L, const uint8_t
     const int64_t want = std::min<int64_t>((int64_t)Mx * Nx, (int64_t)(Vx / 2) * (Vx - Vx / 2));
     const int64_t room = ((int64_t)EX_SMEM_MAX - (int64_t)ex_geom(Vx, 0).bytes - 16) / 4;
     a.g = ex_geom(Vx, (int)std::min(want, room));
-    const bool dbg = getenv("FT_EXACT_DBG") != nullptr;
+    const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_EXACT) != 0;
     const dim3 grid((unsigned)n_per_q, (unsigned)nq);
     cudaError_t e = a.g.Vx <= 256 ? ex_launch<256>(a, grid, st, dbg) : ex_launch<512>(a, grid, st, dbg);
     if (e != cudaSuccess) return e;

@@ -56,7 +56,7 @@ struct FtArgs {
     int use_bitmap;   // query vocab lookup by bitmap + rank (N small enough), else by hash
     int nwords;       // bitmap words = ceil(N / 32)
     unsigned long long* units;   // profiler: Σ pairs (8 s_doc + 16) algorithmic bytes, or null
-    const uint32_t* fb_list;     // list mode: [nq][fb_cap] doc positions handed over by k_ftx
+    const uint32_t* fb_list;     // list mode: [nq][fb_cap] doc positions handed over by k_ftd
     const uint32_t* fb_cnt;      // [nq]
     int64_t fb_cap;
     int32_t q0;                  // first query of this launch (grid.y ≤ 65535)
@@ -64,7 +64,8 @@ struct FtArgs {
 
 constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
 
-constexpr int FT_WARPS = 8;
+constexpr int FT_WARPS = 8;                 // warps per CTA (fewer when the supports are large)
+constexpr size_t FT_SMEM_MAX = 227 * 1024;
 
 struct PairCtx {
     const FtArgs* a;
@@ -359,25 +360,19 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     c.dcum = wsm + 2 * a.Sd;
     c.qres = wsm + 3 * a.Sd;
     c.qcum = wsm + 3 * a.Sd + a.Sq;
-    if (a.tab.table && a.tab.pitch) {
-        c.trow_base = a.tab.table + a.tab.row_base[q];
-        c.tld = (uint32_t)a.tab.pitch[q];
-    } else {
-        c.trow_base = a.tab.table ? a.tab.table + (a.tab.row_base ? a.tab.row_base[q] : (int64_t)q * a.tab.rows_cap) *
-                                                      a.tab.ld
-                                  : nullptr;
-        c.tld = (uint32_t)a.tab.ld;
-    }
+    c.trow_base = a.tab.table ? a.tab.table + a.tab.row_base[q] : nullptr;
+    c.tld = a.tab.table ? (uint32_t)a.tab.pitch[q] : 0u;
     c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
 
     unsigned long long ubytes = 0;
-    // range mode: this CTA's contiguous doc range; list mode: the pairs k_ftx handed over
+    // range mode: this CTA's contiguous doc range; list mode: the pairs k_ftd handed over
     const bool list_mode = a.fb_list != nullptr;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
-    const int64_t e0 = list_mode ? (int64_t)blockIdx.x * FT_WARPS + warp : d0 + warp;
+    const int nwarp = (int)(blockDim.x >> 5);
+    const int64_t e0 = list_mode ? (int64_t)blockIdx.x * nwarp + warp : d0 + warp;
     const int64_t e1 = list_mode ? (int64_t)a.fb_cnt[q] : d1;
-    const int64_t estep = list_mode ? (int64_t)gridDim.x * FT_WARPS : FT_WARPS;
+    const int64_t estep = list_mode ? (int64_t)gridDim.x * nwarp : nwarp;
     for (int64_t e = e0; e < e1; e += estep) {
         const int64_t dp = list_mode ? (int64_t)a.fb_list[(int64_t)q * a.fb_cap + e] : e;
         const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
@@ -497,24 +492,27 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     bx = std::max<int64_t>(bx, 1);
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
-    // FT_VOCAB_HASH=1 (test hook) forces the hash lookup used when N exceeds the bitmap limit
-    a.use_bitmap = (ix->N <= FT_BITMAP_MAX_N && !getenv("FT_VOCAB_HASH")) ? 1 : 0;
+    // FT_OPT_VOCAB_HASH (test option) forces the hash lookup used when N exceeds the bitmap limit
+    a.use_bitmap = (ix->N <= FT_BITMAP_MAX_N && !fti_opt(FT_OPT_VOCAB_HASH)) ? 1 : 0;
     a.nwords = (int)((ix->N + 31) / 32);
     const size_t lookup = a.use_bitmap ? (size_t)a.nwords * 8 : (size_t)L.vh_cap * 8;
     const size_t ysm = a.small_d ? (size_t)a.Sq * a.d * 4 : 0;
-    size_t smem = (size_t)a.Sq * 8 + lookup + ysm + (size_t)FT_WARPS * (3 * a.Sd + 2 * a.Sq) * 4;
+    // per-warp residual arrays: fewer warps per CTA when large supports would exceed the
+    // shared-memory limit (227 KB); FT_ERANGE-class failure when even one warp does not fit
+    const size_t per_warp = (size_t)(3 * a.Sd + 2 * a.Sq) * 4;
+    const size_t fixed = (size_t)a.Sq * 8 + lookup + ysm;
+    int warps = FT_WARPS;
+    while (warps > 1 && fixed + warps * per_warp > FT_SMEM_MAX) warps--;
+    if (fixed + warps * per_warp > FT_SMEM_MAX) return cudaErrorInvalidConfiguration;
+    const size_t smem = fixed + warps * per_warp;
     cudaError_t e;
-    // with a distance table and a star-like tree, the lane-per-pair kernel (ft_flowd.cu; or, for
-    // exhaustive scoring with FT_FTX=1, the lane-per-query chunk kernel ft_flowx.cu) scores every
-    // pair it can and lists the rest for this kernel (list mode)
-    if (!d_flow && tab.table && a.use_bitmap && ds->n_mn <= 2 * ds->n && L.smax <= FTX_MAX_SQ &&
-        !getenv("FT_GENERAL_ONLY")) {
+    // with a distance table and a star-like tree, the lane-per-pair kernel (ft_flowd.cu) scores
+    // every pair it can and lists the rest for this kernel (list mode)
+    if (!d_flow && tab.table && a.use_bitmap && ds->n_mn <= 2 * ds->n && L.smax <= FTD_MAX_SQ &&
+        !fti_opt(FT_OPT_WARP_ONLY)) {
         uint32_t* fl = nullptr;
         uint32_t* fc = nullptr;
-        if (!d_docs && !tab.map && getenv("FT_FTX"))
-            e = fti_launch_ftx(ds, L, d_qblock, nq, n_docs, tab, d_out, out_ld, &fl, &fc, st);
-        else
-            e = fti_launch_ftd(ds, L, d_qblock, nq, d_docs, docs_ld, n_docs, tab, d_out, out_ld, &fl, &fc, st);
+        e = fti_launch_ftd(ds, L, d_qblock, nq, d_docs, docs_ld, n_docs, tab, d_out, out_ld, &fl, &fc, st);
         if (e == cudaSuccess) {
             a.fb_list = fl;
             a.fb_cnt = fc;
@@ -529,7 +527,7 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     if (e != cudaSuccess) return e;
     for (int32_t q0 = 0; q0 < nq; q0 += 65535) {          // grid.y ≤ 65535 queries per launch
         a.q0 = q0;
-        kern<<<dim3((unsigned)bx, (unsigned)std::min(65535, nq - q0)), FT_WARPS * 32, smem, st>>>(a);
+        kern<<<dim3((unsigned)bx, (unsigned)std::min(65535, nq - q0)), warps * 32, smem, st>>>(a);
         fti_count_launches(1);
     }
     return cudaGetLastError();

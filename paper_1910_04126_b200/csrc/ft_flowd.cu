@@ -56,10 +56,9 @@ struct DArgs {
     int64_t docs_ld, n_docs, n;
     const float* table;
     const uint2* map;          // [nq][nw] {bits, rank} rows of the compact table, or null (row = vocab id)
-    const int64_t* row_base;   // [nq] or null (q * rows_cap)
-    const int32_t* pitch;      // [nq] per-query pitch (row_base in elements), or null
+    const int64_t* row_base;   // [nq] ELEMENT offset of each query's table
+    const int32_t* pitch;      // [nq] per-query row pitch (floats)
     int64_t rows_cap;
-    int32_t ld;
     int32_t nw, Sq;
     double* out;
     int64_t out_ld;
@@ -112,9 +111,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint16_t* myq = queue + warp * DCAP * 32 + lane;
-    const float* trow = a.pitch ? a.table + a.row_base[q]
-                                : a.table + (a.row_base ? a.row_base[q] : (int64_t)q * a.rows_cap) * a.ld;
-    const uint32_t ld = (uint32_t)(a.pitch ? a.pitch[q] : a.ld);
+    const float* trow = a.table + a.row_base[q];
+    const uint32_t ld = (uint32_t)a.pitch[q];
     const bool smap_on = a.map != nullptr;
     const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
     (void)gmapq;
@@ -380,17 +378,25 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.qblock = d_qblock; a.L = L;
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;
     a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.pitch = tab.pitch; a.rows_cap = tab.rows_cap;
-    a.ld = tab.ld;
     a.out = d_out; a.out_ld = out_ld;
     a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;
     a.err = ds->err_dev;
     a.units = ds->units_ptr(FTI_ST_FT);
-    // function attributes are set only when they change
-    static int cur_smem = -1, cur_pct = -1;
-    if ((int)smem > cur_smem) {
+    // function attributes are per device; they are set only when they change
+    constexpr int MAXDEV = 64;
+    static thread_local int cur_smem[MAXDEV], cur_pct[MAXDEV];
+    static thread_local bool init = false;
+    if (!init) {
+        for (int i = 0; i < MAXDEV; i++) cur_smem[i] = cur_pct[i] = -1;
+        init = true;
+    }
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if (dev >= MAXDEV) return cudaErrorInvalidDevice;
+    if ((int)smem > cur_smem[dev]) {
         if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
-        cur_smem = (int)smem;
+        cur_smem[dev] = (int)smem;
     }
     // the L1 caches the lanes' doc records between the pre-pass and the merge: give shared memory
     // only what the target CTAs per SM need (3, or 2 with the 25 KB-class candidate row map)
@@ -398,12 +404,12 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
         const int ctas = tab.map && !FTD_GMAP ? 2 : FTD_MINB;
         const size_t need = (size_t)ctas * (smem + 2176 + 1024);
         int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
-        if (const char* ev = getenv("FT_FTD_CARVEOUT")) pct = atoi(ev);
+        if (fti_opt(FT_OPT_FTD_CARVEOUT) > 0) pct = (int)fti_opt(FT_OPT_FTD_CARVEOUT);
         pct = std::min(100, pct);
-        if (pct != cur_pct) {
+        if (pct != cur_pct[dev]) {
             if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess)
                 return e;
-            cur_pct = pct;
+            cur_pct[dev] = pct;
         }
     }
     const int64_t gx = (n_docs + DW * 32 - 1) / (DW * 32);

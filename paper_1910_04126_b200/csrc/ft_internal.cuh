@@ -42,6 +42,13 @@ ft_status fti_fail(ft_status st, const std::string& msg);
             return fti_fail(FT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
     } while (0)
 
+// process-wide options set through ft_set_option (include/flowtree.h); 0 = default
+int64_t fti_opt(int option);
+#define FTI_DBG_DIST 1
+#define FTI_DBG_EXACT 2
+#define FTI_DBG_SELECT 4
+#define FTI_DBG_ALLOC 8
+
 // grow-only device buffer
 struct DevBuf {
     void* p = nullptr;
@@ -52,7 +59,7 @@ struct DevBuf {
         p = nullptr;
         bytes = 0;
         size_t nb = b < 256 ? 256 : b;
-        if (getenv("FT_ALLOC_DBG")) fprintf(stderr, "ft DevBuf grow -> %zu bytes\n", nb);
+        if (fti_opt(FT_OPT_DEBUG) & FTI_DBG_ALLOC) fprintf(stderr, "ft DevBuf grow -> %zu bytes\n", nb);
         cudaError_t e = cudaMalloc(&p, nb);
         if (e == cudaSuccess) bytes = nb;
         return e;
@@ -154,7 +161,7 @@ struct ft_dataset {
     unsigned long long* units_ptr(int stage) const { return prof ? prof_units + stage : nullptr; }
     // scratch (grow-only; reused across calls)
     DevBuf s_pitch, s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
-    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_ftxchunk;
+    DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_topk;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -170,24 +177,19 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
                           cudaStream_t st);
 struct FtTable {
-    const float* table = nullptr;      // rows of ld floats, or null (on-the-fly distances)
-    const uint2* map = nullptr;        // [nq][ceil(N/32)] {bits, rank}: row = rank + popc(bits below), or null
-    const int64_t* row_base = nullptr; // [nq] first row of each query (compact), or null (q * rows_cap)
-    const int32_t* pitch = nullptr;    // [nq] per-query row pitch; then row_base is an ELEMENT offset
+    const float* table = nullptr;      // query tables, or null (on-the-fly distances)
+    const uint2* map = nullptr;        // [nq][ceil(N/32)] {bits, rank}: row = rank + popc(bits below), or null (row = vocab id)
+    const int64_t* row_base = nullptr; // [nq] ELEMENT offset of each query's table
+    const int32_t* pitch = nullptr;    // [nq] row pitch (floats) of each query's table
     int64_t rows_cap = 0;
-    int32_t ld = 0;
 };
-// exhaustive Flowtree, lane = query of a 32-query chunk (ft_flowx.cu); pairs it cannot score are
-// listed per query in *fb_list / *fb_cnt (capacity n_docs per query) for the warp kernel
-#define FTX_MAX_SQ 256
-// lane-per-pair Flowtree with a distance table (ft_flowd.cu), candidate lists or all docs; the
-// pairs it cannot score are listed the same way
+// lane-per-pair Flowtree with a distance table (ft_flowd.cu), candidate lists or all docs; pairs it
+// cannot score are listed per query in *fb_list / *fb_cnt (capacity n_docs per query) for the
+// warp kernel's list mode.  Query supports up to FTD_MAX_SQ.
+#define FTD_MAX_SQ 255
 cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                            const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
                            int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st);
-cudaError_t fti_launch_ftx(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t n_docs,
-                           const FtTable& tab, double* d_out, int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt,
-                           cudaStream_t st);
 // exact W1 of per-query candidate lists by the transportation simplex (ft_exact.cu)
 cudaError_t fti_launch_exact(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                              const int64_t* d_docs, int64_t docs_ld, int64_t n_per_q, double* d_out, int64_t out_ld,
@@ -198,13 +200,10 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           cudaStream_t st);
 cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
-                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, int32_t ld,
-                                  cudaStream_t st);
+                                  const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, cudaStream_t st);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  cudaStream_t st);
-cudaError_t fti_launch_row_base(const int32_t* d_rowcnt, const uint8_t* d_qblock, const QueryLayout& L, int32_t nq,
-                                int64_t* d_row_base, int32_t* d_pitch, cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
                               int* d_scratch /* rows + 1 ints */, cudaStream_t st, int64_t id_base = 0);

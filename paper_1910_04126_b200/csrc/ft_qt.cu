@@ -527,7 +527,7 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     dg.mw = (int)((ds->ix->M + 31) / 32);
     const size_t dense_budget = 200 * 1024;
     dg.cap = 0;
-    if ((size_t)dg.mw * 8 <= 96 * 1024 && !getenv("FT_QT_HASH"))   // FT_QT_HASH=1: test hook, hash path only
+    if ((size_t)dg.mw * 8 <= 96 * 1024 && !fti_opt(FT_OPT_QT_HASH))   // FT_OPT_QT_HASH: test option, hash path only
         dg.cap = (int)std::min<size_t>(2048, (dense_budget - (size_t)dg.mw * 8) / (QT_QC * 2)) & ~31;
     dg.stride = (sizeof(DenseHdr) + (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 15) / 16 * 16;
     if (dg.cap > 0) {
@@ -558,8 +558,9 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     int ctas_per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_qt, QT_WARPS * 32, smem);
     ctas_per_sm = std::max(1, ctas_per_sm);
-    int waves = 8;   // CTAs per SM slot over the launch (measured: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews batch); FT_QT_WAVES tunes it
-    if (const char* ev = getenv("FT_QT_WAVES")) waves = std::max(1, atoi(ev));
+    // CTAs per SM slot over the launch (measured: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews
+    // batch); FT_OPT_QT_WAVES tunes it
+    const int waves = fti_opt(FT_OPT_QT_WAVES) > 0 ? (int)fti_opt(FT_OPT_QT_WAVES) : 8;
     const int64_t target = (int64_t)148 * ctas_per_sm * waves;
     int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + nchunks - 1) / nchunks));
     a.docs_per_cta = (n_docs + bx - 1) / bx;

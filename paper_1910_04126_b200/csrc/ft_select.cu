@@ -473,7 +473,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     size_t smem = (size_t)P * 12 + 16;
     cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (getenv("FT_SELECT_RADIX")) {   // test hook: the radix kernel for every row
+    if (fti_opt(FT_OPT_SELECT_RADIX)) {   // test option: the radix kernel for every row
         k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P,
                                           nullptr, nullptr, id_base);
         fti_count_launches(1);
@@ -485,7 +485,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     e = cudaMemsetAsync(nredo, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     const size_t smem_f = (size_t)SEL_CAP * 12;
-    const bool dbg = getenv("FT_SELECT_DBG") != nullptr;
+    const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_SELECT) != 0;
     auto kf = L > SEL_CAP ? (dbg ? k_select_fast<true, 16> : k_select_fast<false, 16>)
                           : (dbg ? k_select_fast<true, 2> : k_select_fast<false, 2>);
     e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);

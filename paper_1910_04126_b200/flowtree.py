@@ -29,8 +29,12 @@ EXPORTED = ["ft_build_quadtree", "ft_build_quadtree_shift", "ft_index_info", "ft
             "ft_synchronize", "ft_index_free", "ft_dataset_free", "ft_last_error",
             "ft_profile_enable", "ft_profile_reset", "ft_profile_read", "ft_profile_units",
             "ft_profile_stage_name", "ft_launch_count", "ft_topk", "ft_flowtree_estimate_lists",
-            "ft_exact_w1_lists"]
+            "ft_exact_w1_lists", "ft_set_option", "ft_get_option"]
 FT_NUM_STAGES = 7
+# ft_set_option keys (include/flowtree.h)
+(FT_OPT_VOCAB_HASH, FT_OPT_WARP_ONLY, FT_OPT_QT_HASH, FT_OPT_SELECT_RADIX, FT_OPT_EXACT_START_NW,
+ FT_OPT_TABLE_CHUNK, FT_OPT_TABLE_BUDGET_MB, FT_OPT_QT_WAVES, FT_OPT_FTD_CARVEOUT, FT_OPT_DEBUG) = range(10)
+FT_NUM_OPTIONS = 10
 FT_PROF_DIST_FLOPS = FT_NUM_STAGES   # ft_profile_units slot: distance-table algorithmic flops
 
 
@@ -74,6 +78,8 @@ def _load_lib():
         "ft_topk": (st, [P, i64, P, i64, i64, i64, i32, i32, P, P, P]),
         "ft_flowtree_estimate_lists": (st, [P, P, i32, P, P, P, i64, i64, P, P]),
         "ft_exact_w1_lists": (st, [P, P, i32, P, P, P, i64, i64, P, P]),
+        "ft_set_option": (st, [i32, i64]),
+        "ft_get_option": (st, [i32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -337,6 +343,16 @@ def ft_profile_units(ds, stage: int) -> int:
 
 def ft_profile_stage_name(stage: int) -> str:
     return _lib.ft_profile_stage_name(stage).decode()
+
+
+def ft_set_option(option: int, value: int):
+    _check(_lib.ft_set_option(int(option), int(value)))
+
+
+def ft_get_option(option: int) -> int:
+    v = ctypes.c_int64(0)
+    _check(_lib.ft_get_option(int(option), ctypes.byref(v)))
+    return v.value
 
 
 def ft_launch_count() -> int:

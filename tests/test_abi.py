@@ -70,3 +70,17 @@ def test_host_errors_without_gpu(lib):
     lib.ft_knn.restype = ctypes.c_int
     rc = lib.ft_knn(None, None, 1, None, None, 5, 0, None, None, None)
     assert rc == 6                                   # FT_ESTATE: NULL dataset
+
+
+def test_options_roundtrip_without_gpu():
+    """ft_set_option / ft_get_option (test and tuning options, no environment reads) work on the
+    host and reject unknown keys and out-of-range values."""
+    from paper_1910_04126_b200 import flowtree as ft
+    for o in range(ft.FT_NUM_OPTIONS):
+        assert ft.ft_get_option(o) == 0
+    ft.ft_set_option(ft.FT_OPT_TABLE_CHUNK, 3)
+    assert ft.ft_get_option(ft.FT_OPT_TABLE_CHUNK) == 3
+    ft.ft_set_option(ft.FT_OPT_TABLE_CHUNK, 0)
+    for bad in [(ft.FT_NUM_OPTIONS, 1), (-1, 1), (ft.FT_OPT_DEBUG, -1), (ft.FT_OPT_FTD_CARVEOUT, 101)]:
+        with pytest.raises(ft.FlowtreeError):
+            ft.ft_set_option(*bad)

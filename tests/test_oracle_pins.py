@@ -24,6 +24,19 @@ def test_splitmix64_reference_vector():
     assert got == [int(v) for v in g["outputs"]]
 
 
+def test_sigma_from_seed_golden():
+    """O2's seed → σ mapping pinned to σ computed by hand from the PUBLISHED SplitMix64 outputs
+    (tests/golden/sigma_from_seed.json, exact rational arithmetic, reading R3).  A
+    wrong shift (z >> 12), scale, or output index fails it."""
+    g = H.golden("sigma_from_seed.json")
+    for c in g["cases"]:
+        X = np.zeros((2, g["d"]), np.float32)
+        X[1, :] = np.float32(c["phi_f32"])
+        T = oracle.Tree(X, seed=g["seed"], max_depth=8)
+        assert T.phi == float.fromhex(c["phi"])
+        assert [float(v) for v in T.sigma] == [float.fromhex(h) for h in c["sigma"]], c["phi_f32"]
+
+
 def test_sigma_in_range_and_deterministic():
     X = np.random.default_rng(0).standard_normal((50, 7)).astype(np.float32)
     a = oracle.Tree(X, seed=99)

@@ -29,6 +29,16 @@ def ft():
     return flowtree
 
 
+@pytest.fixture
+def opt(ft):
+    """Set library options (ft_set_option) for one test; every option is reset to 0 afterwards."""
+    def set_(name, value=1):
+        ft.ft_set_option(getattr(ft, name), value)
+    yield set_
+    for o in range(ft.FT_NUM_OPTIONS):
+        ft.ft_set_option(o, 0)
+
+
 _TREES = {}
 
 
@@ -206,14 +216,14 @@ def test_doc_subset_and_self_queries(ft):
             assert_ft_close([fl[qi, j]], [T.ft(*wl.doc(dd), ids_, w_)])
 
 
-def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
+def test_vocab_hash_path_matches_bitmap(ft, opt):
     """The Flowtree kernel looks query vocab up by bitmap (N ≤ 2^19) or hash (larger N); both
-    must give identical values and flows (FT_VOCAB_HASH=1 forces the hash)."""
+    must give identical values and flows (FT_OPT_VOCAB_HASH forces the hash)."""
     wl = get_workload("image", n_docs=300, n_queries=3)
     ix, ds = _setup(ft, wl)
     a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
     f_a = ds.flow(*wl.query(1), 17)
-    monkeypatch.setenv("FT_VOCAB_HASH", "1")
+    opt("FT_OPT_VOCAB_HASH")
     b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
     f_b = ds.flow(*wl.query(1), 17)
     assert np.array_equal(a, b)
@@ -222,15 +232,15 @@ def test_vocab_hash_path_matches_bitmap(ft, monkeypatch):
 
 
 @pytest.mark.parametrize("name,nq", [("text", 40), ("reviews", 70)])
-def test_chunked_flowtree_matches_warp_kernel(ft, monkeypatch, name, nq):
+def test_chunked_flowtree_matches_warp_kernel(ft, opt, name, nq):
     """Exhaustive scoring runs the lane-per-pair kernel k_ftd (pairs sharing an M-node are listed
-    for the warp kernel); FT_GENERAL_ONLY=1 runs the warp kernel for every pair.  The flows are the
+    for the warp kernel); FT_OPT_WARP_ONLY runs the warp kernel for every pair.  The flows are the
     same triples, so the values agree to FP summation order; ragged chunks (nq not a multiple of
     32) included."""
     wl = get_workload(name, n_docs=2500, n_queries=nq)
     ix, ds = _setup(ft, wl)
     a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
-    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    opt("FT_OPT_WARP_ONLY")
     b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
     assert np.all(np.isfinite(a))
     np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
@@ -239,10 +249,10 @@ def test_chunked_flowtree_matches_warp_kernel(ft, monkeypatch, name, nq):
 
 @pytest.mark.parametrize("name,nq,mode", [("text", 40, "lists"), ("reviews", 70, "lists"), ("reviews", 9, "all"),
                                            ("stress", 5, "lists")])
-def test_lane_per_pair_flowtree_matches_other_kernels(ft, monkeypatch, name, nq, mode):
+def test_lane_per_pair_flowtree_matches_other_kernels(ft, opt, name, nq, mode):
     """The lane-per-pair kernel (k_ftd: 32 pairs of one query per warp, pairs with a common M-node
     or more than 32 shared ids listed for the warp kernel) against the warp kernel for every pair
-    (FT_GENERAL_ONLY=1) and, over all docs, the lane-per-query chunk kernel (FT_FTX=1).  Candidate
+    (FT_OPT_WARP_ONLY).  Candidate
     lists (mode "lists") hold repeats and a ragged tail, as the pipeline's top-m rows do."""
     wl = get_workload(name, n_docs=3000, n_queries=nq)
     ix, ds = _setup(ft, wl)
@@ -251,16 +261,11 @@ def test_lane_per_pair_flowtree_matches_other_kernels(ft, monkeypatch, name, nq,
         rng = np.random.default_rng(5)
         docs = np.concatenate([rng.choice(wl.n, 700, replace=False), [0, wl.n - 1, 0]]).astype(np.int64)
     a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
-    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    opt("FT_OPT_WARP_ONLY")
     b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
-    monkeypatch.delenv("FT_GENERAL_ONLY")
     assert np.all(np.isfinite(a))
     np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
     assert np.array_equal(a == 0.0, b == 0.0)
-    if mode == "all":
-        monkeypatch.setenv("FT_FTX", "1")
-        c = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
-        np.testing.assert_allclose(a, c, rtol=1e-6, atol=0)
 
 
 @pytest.mark.parametrize("big", [False, True])
@@ -312,7 +317,7 @@ def test_flowtree_degenerate_and_maximum_supports(ft, big):
 
 
 @pytest.mark.parametrize("max_depth", [1, 2])
-def test_lane_per_pair_flowtree_capped_tree(ft, monkeypatch, max_depth):
+def test_lane_per_pair_flowtree_capped_tree(ft, opt, max_depth):
     """A depth cap that binds (d = 300 mixture, D = 1 or 2) puts many points into multi-point
     leaves and M-nodes: the lane-per-pair kernel must hand every pair whose flow matches at an
     M-node (or at a multi-point leaf holding a shared id) to the warp kernel and score the rest as
@@ -325,7 +330,7 @@ def test_lane_per_pair_flowtree_capped_tree(ft, monkeypatch, max_depth):
     docs = rng.choice(wl.n, 600, replace=False).astype(np.int64)
     a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
     full = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
-    monkeypatch.setenv("FT_GENERAL_ONLY", "1")
+    opt("FT_OPT_WARP_ONLY")
     b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=docs)
     fb = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
     np.testing.assert_allclose(a, b, rtol=1e-6, atol=0)
@@ -335,14 +340,14 @@ def test_lane_per_pair_flowtree_capped_tree(ft, monkeypatch, max_depth):
 
 
 @pytest.mark.parametrize("name", ["image", "text", "reviews"])
-def test_qt_dense_matches_hash(ft, monkeypatch, name):
+def test_qt_dense_matches_hash(ft, opt, name):
     """The Quadtree kernel scans a chunk with the dense bitmap structure when its node union is
-    small and with the hash structure otherwise (FT_QT_HASH=1 forces the hash); both are exact,
+    small and with the hash structure otherwise (FT_OPT_QT_HASH forces the hash); both are exact,
     so the values must be bit-identical (the oracle comparison is in the parity tests)."""
     wl = get_workload(name, n_docs=3000, n_queries=40)
     ix, ds = _setup(ft, wl)
     a = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
-    monkeypatch.setenv("FT_QT_HASH", "1")
+    opt("FT_OPT_QT_HASH")
     b = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
     assert np.array_equal(a, b)
 
@@ -397,12 +402,12 @@ def test_knn_tiny(ft, prefilter_m):
 
 
 @pytest.mark.parametrize("n_docs,radix", [(5000, False), (20000, False), (20000, True)])
-def test_knn_prefilter_ids_exact(ft, monkeypatch, n_docs, radix):
+def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix):
     """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id), in
     order.  n ≤ 8192 sorts the whole row; n = 20000 takes the sample-threshold path (the Quadtree
-    values at d = 300 are heavily tied); FT_SELECT_RADIX=1 forces the MSD radix kernel."""
+    values at d = 300 are heavily tied); FT_OPT_SELECT_RADIX forces the MSD radix kernel."""
     if radix:
-        monkeypatch.setenv("FT_SELECT_RADIX", "1")
+        opt("FT_OPT_SELECT_RADIX")
     wl = get_workload("reviews", n_docs=n_docs, n_queries=4)
     T = oracle_tree(wl)
     ix, ds = _setup(ft, wl)
@@ -586,14 +591,14 @@ def test_topk_large_rows_rank_select(ft, L, k, levels):
 @pytest.mark.parametrize("start", ["greedy", "nw"])
 @pytest.mark.parametrize("name,nd,nq,per_q", [("reviews", 3000, 6, 12), ("tiny", 100, 4, 10), ("text", 800, 3, 6),
                                               ("image", 300, 2, 5)])
-def test_exact_w1_matches_lp(ft, name, nd, nq, per_q, start, monkeypatch):
+def test_exact_w1_matches_lp(ft, name, nd, nq, per_q, start, opt):
     """Transportation simplex per (query, doc) against the oracle's exact W1 (LP, FP64 costs):
     within 1e-6 relative (FP32 costs); exact ≤ Flowtree; negative entries score +inf.  Both starting
     bases (mutual-minimum rounds, plain northwest corner) reach the same optimum; image pairs
     (170 + 170 points) take the 512-thread variant."""
     import torch
     if start == "nw":
-        monkeypatch.setenv("FT_EXACT_START", "nw")
+        opt("FT_OPT_EXACT_START_NW")
     wl = get_workload(name, n_docs=nd, n_queries=nq)
     ix, ds = _setup(ft, wl)
     rng = np.random.default_rng(11)
@@ -694,13 +699,13 @@ def test_more_than_65535_queries(ft):
             assert abs(ex[q, j] - w1) <= 1e-6 * w1, (q, d)
 
 
-def test_knn_table_chunking_invariant(ft, monkeypatch):
+def test_knn_table_chunking_invariant(ft, opt):
     """The distance tables are built per query chunk (the chunk size follows the free HBM); any
-    chunking gives bit-identical k-NN ids and values (FT_TABLE_CHUNK forces ragged chunks of 3)."""
+    chunking gives bit-identical k-NN ids and values (FT_OPT_TABLE_CHUNK forces ragged chunks of 3)."""
     wl = get_workload("reviews", n_docs=3000, n_queries=11)
     ix, ds = _setup(ft, wl)
     ids0, v0 = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 300)
-    monkeypatch.setenv("FT_TABLE_CHUNK", "3")
+    opt("FT_OPT_TABLE_CHUNK", 3)
     ids1, v1 = ds.knn(wl.q_off, wl.q_ids, wl.q_w, 10, 300)
     assert np.array_equal(ids0, ids1) and np.array_equal(v0, v1)
 

@@ -1,5 +1,5 @@
 """Time the exact-W1 stage on its own (1000 queries x 9 docs of a workload) and, with
-FT_EXACT_DBG=1, print the per-CTA cycle split (cost matrix / pointer jumping / pricing / cycle)."""
+FT_OPT_DEBUG bit 2, print the per-CTA cycle split (cost matrix / pointer jumping / pricing / cycle)."""
 import os, sys, time
 import numpy as np
 import torch
@@ -15,7 +15,7 @@ rng = np.random.default_rng(0)
 docs = torch.from_numpy(rng.integers(0, ds.n, (wl.nq, 9))).cuda()
 for dbg in (False, True):
     if dbg:
-        os.environ["FT_EXACT_DBG"] = "1"
+        ft.ft_set_option(ft.FT_OPT_DEBUG, 2)
     for _ in range(2):
         out = ft.ft_exact_w1_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, docs)
     torch.cuda.synchronize()

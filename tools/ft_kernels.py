@@ -1,7 +1,7 @@
 """Flowtree-stage times of the kernel variants (reviews-like unless given):
 python tools/ft_kernels.py [config] [knn_queries] [exhaustive_queries]
-default = lane-per-pair k_ftd (+ warp kernel list mode); FT_FTX=1 = lane-per-query k_ftx for
-exhaustive scoring; FT_GENERAL_ONLY=1 = warp kernel for every pair."""
+default = lane-per-pair k_ftd (+ warp kernel list mode); FT_OPT_WARP_ONLY = warp kernel for every
+pair."""
 import os, sys
 import numpy as np
 import torch
@@ -24,12 +24,10 @@ sw = torch.from_numpy(sub.q_w.view(np.int32)).cuda().view(torch.uint32)
 out = torch.empty((sub.nq, wl.n), dtype=torch.float64, device="cuda")
 res = {}
 only = sys.argv[4].split(",") if len(sys.argv) > 4 else None
-for var, env in (("ftd", {}), ("ftx", {"FT_FTX": "1"}), ("warp", {"FT_GENERAL_ONLY": "1"})):
+for var, warp_only in (("ftd", 0), ("warp", 1)):
     if only and var not in only:
         continue
-    for k in ("FT_FTX", "FT_GENERAL_ONLY"):
-        os.environ.pop(k, None)
-    os.environ.update(env)
+    ft.ft_set_option(ft.FT_OPT_WARP_ONLY, warp_only)
     m = wl.prefilter_m if wl.prefilter_m else 0
     ds.knn(wl.q_off, qi, qw, wl.k, m, out_ids=oi, out_val=ov)
     ft.ft_profile_enable(ds.h, True)
@@ -53,7 +51,7 @@ for var, env in (("ftd", {}), ("ftx", {"FT_FTX": "1"}), ("warp", {"FT_GENERAL_ON
           f"({sub.nq} q x {wl.n} docs = {sub.nq * wl.n / ex / 1e6:.3f} G pairs/s); dist {p.get('dist_table', (0,))[0]/3:.3f} ms",
           flush=True)
 a = res["ftd"][2]
-for v in [v for v in ("ftx", "warp") if v in res]:
+for v in [v for v in ("warp",) if v in res]:
     b = res[v][2]
     print(v, "max rel diff vs ftd", float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))),
           "knn ids equal", bool(np.array_equal(res[v][3], res["ftd"][3])))

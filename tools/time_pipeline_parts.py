@@ -18,5 +18,5 @@ print("pipeline", tm(lambda: pipeline.knn_qt_ft_exact(ft, ds, wl.q_off, qi, qw, 
 i2 = torch.empty((1000, 10), dtype=torch.int64, device="cuda"); v2 = torch.empty((1000, 10), dtype=torch.float64, device="cuda")
 print("knn(10,1000)", tm(lambda: ds.knn(wl.q_off, qi, qw, 10, 1000, out_ids=i2, out_val=v2)))
 for c in ("3", "48"):
-    os.environ["FT_TABLE_BUDGET_GB"] = c
+    ft.ft_set_option(ft.FT_OPT_TABLE_BUDGET_MB, int(c) * 1024)
     print("budget", c, "knn(9,424)", tm(lambda: ds.knn(wl.q_off, qi, qw, 9, 424, out_ids=ids, out_val=vals)))
