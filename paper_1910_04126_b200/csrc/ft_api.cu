@@ -217,7 +217,9 @@ ft_status stage_docs(ft_dataset* ds, const int64_t* docs, int64_t n_docs, cudaSt
 ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int64_t* d_docs, int64_t docs_ld,
                          int64_t n_docs, double* d_out, int64_t out_ld, cudaStream_t st) {
     const ft_index* ix = ds->ix;
-    if (ix->d <= FTI_SMALL_D) {
+    if (ix->d <= FTI_SMALL_D || !fti_dist_supported(ix)) {
+        // small d: distances on the fly from shared memory; d beyond the distance-table kernel's
+        // shared-memory geometry (> 576): on the fly from global memory (slow, any d)
         StageTimer tm(ds, FTI_ST_FT, st);
         FTI_FT(fti_launch_ft(ds, S.L, S.qblock, nq, d_docs, docs_ld, n_docs, FtTable{}, d_out, out_ld, nullptr,
                              nullptr, 0, st));

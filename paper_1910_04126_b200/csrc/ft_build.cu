@@ -457,6 +457,6 @@ extern "C" ft_status ft_index_nodes(const ft_index* ix, int32_t* depth, int32_t*
 extern "C" void ft_index_free(ft_index* ix) {
     if (!ix) return;
     cudaFree(ix->X); cudaFree(ix->path); cudaFree(ix->leaf_depth); cudaFree(ix->node_depth);
-    cudaFree(ix->node_count); cudaFree(ix->vflags); cudaFree(ix->Xc); cudaFree(ix->xnorm);
+    cudaFree(ix->node_count); cudaFree(ix->vflags); cudaFree(ix->Xq); cudaFree(ix->xnq);
     delete ix;
 }

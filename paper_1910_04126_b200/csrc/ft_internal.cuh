@@ -93,10 +93,13 @@ struct ft_index {
     int32_t* node_count = nullptr;    // [M] ground points in the cell
     uint32_t* vflags = nullptr;       // [N] FTI_FLAG_* per ground point
     // distance-table operand (built on first use, ft_dist.cu): the points translated by their FP64
-    // mean, FP32, rows padded to dpad (a multiple of 32) and one extra all-zero row N; their norms
-    float* Xc = nullptr;              // [(N+1)*dpad]
-    float* xnorm = nullptr;           // [N+1] ||x − mean||^2
-    int32_t dpad = 0;
+    // mean and quantised to 24-bit fixed point v = rint((x − mean)·2^qexp), stored as three signed
+    // 8-bit limbs per coordinate (v = a0 + 2^8 a1 + 2^16 a2), rows [nks][3 limbs][64 bytes] with
+    // the coordinates zero padded to 64·nks and one extra all-zero row N; exact int64 norms Σ v²
+    int8_t* Xq = nullptr;             // [(N+1) * nks * 192]
+    long long* xnq = nullptr;         // [N+1]
+    int32_t nks = 0;                  // 64-coordinate K stages
+    int32_t qexp = 0;                 // quantisation exponent e
     int device = 0;
 };
 
@@ -201,6 +204,8 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
 cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                                   const int32_t* d_rows, const int32_t* d_rowcnt, int64_t rows_cap,
                                   const int64_t* d_row_base, const int32_t* d_pitch, float* d_table, cudaStream_t st);
+// the distance-table kernel's shared-memory geometry holds this index's dimension (d ≤ 576)
+bool fti_dist_supported(const ft_index* ix);
 cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t* d_cand, int64_t cand_ld,
                                  int64_t n_cand, uint2* d_map, int32_t* d_rows, int32_t* d_rowcnt, int64_t rows_cap,
                                  cudaStream_t st);

@@ -354,12 +354,13 @@ def test_qt_dense_matches_hash(ft, opt, name):
 
 def test_distance_table_accuracy(ft):
     """FT(δ_x, δ_y) = ||x − y|| (one triple), so single-point docs/queries expose the tensor-core
-    distance table directly; compare with FP64 distances.  Error model: the Gram
-    form ||x̃||² + ||ỹ||² − 2 x̃·ỹ over the mean-translated points with a 3xTF32 dot accumulated in
-    FP32 errs by at most ~2^-15 (||x̃||² + ||ỹ||²) in d²; ids shared by both sides are exactly 0."""
+    distance table directly; compare with FP64 distances.  Error model: the table is
+    the exact distance between the points quantised to 24-bit fixed point (unit 2^-e, e the largest
+    exponent with max|x − mean|·2^e ≤ 2^23 − 2^16), so |D − ||x − y||| ≤ sqrt(d)·2^-e, plus ≈2^-23
+    relative from the FP32 conversion and square root; ids shared by both sides are exactly 0."""
     wl = get_workload("reviews", n_docs=64, n_queries=2)
     rng = np.random.default_rng(3)
-    N = wl.X.shape[0]
+    N, d = wl.X.shape
     xs = rng.choice(N, 3000, replace=False).astype(np.int32)
     ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
     ds = ft.Dataset(ix, np.arange(len(xs) + 1, dtype=np.int64), xs, np.ones(len(xs), np.uint32))
@@ -369,14 +370,64 @@ def test_distance_table_accuracy(ft):
     ref = np.sqrt(((Xd[ys][:, None, :] - Xd[xs][None, :, :]) ** 2).sum(-1))
     same = ys[:, None] == xs[None, :]
     assert same.any() and np.all(got[same] == 0.0)
-    mu = Xd.mean(0)
-    nrm = ((Xd - mu) ** 2).sum(1)
-    scale = nrm[ys][:, None] + nrm[xs][None, :]
-    err_d2 = np.abs(got.astype(np.float64) ** 2 - ref ** 2)
-    assert np.all(err_d2[~same] <= 2.0 ** -15 * scale[~same]), (err_d2 / scale)[~same].max()
-    rel = np.abs(got - ref)[~same] / ref[~same]
-    assert np.median(rel) < 2e-7, np.median(rel)
-    assert rel.max() < 1e-4, rel.max()
+    M = np.abs(Xd - Xd.mean(0)).max()
+    unit = 2.0 * M / ((1 << 23) - (1 << 16))          # ≥ 2^-e
+    err = np.abs(got.astype(np.float64) - ref)
+    assert np.all(err <= np.sqrt(d) * unit + 3e-7 * ref), (err - 3e-7 * ref).max() / unit
+    rel = err[~same] / ref[~same]
+    assert np.median(rel) < 5e-8, np.median(rel)
+    assert rel.max() < 1e-6, rel.max()
+
+
+def test_distance_table_near_pairs_and_duplicates(ft):
+    """The pairs a Gram-form table gets wrong: nearest neighbours (the same mixture component,
+    d² ≈ 50 against ||x̃||² + ||ỹ||² ≈ 600) and duplicated coordinates under distinct ids, in
+    one- to three-point supports with non-uniform weights, through the d = 300 table path.  Every
+    pair against the oracle at the 1e-5 bar; oracle 0 (identical coordinates) ⇒ GPU exactly 0."""
+    base = get_workload("reviews", n_docs=64, n_queries=2)
+    X = base.X.copy()
+    N = len(X)
+    dup_src, dup_dst = np.arange(20), N - 1 - np.arange(20)
+    X[dup_dst] = X[dup_src]                                   # distinct ids, identical coordinates
+    rng = np.random.default_rng(11)
+    Xd = X.astype(np.float64)
+    qpts = rng.choice(N - 100, 24, replace=False)
+    near = []
+    for y in qpts:
+        d2 = ((Xd - Xd[y]) ** 2).sum(1)
+        d2[y] = np.inf
+        near.append(np.argsort(d2)[:12])
+    docs, dws = [], []
+    for y, nn in zip(qpts, near):
+        for x in nn[:5]:
+            docs.append([int(x)]); dws.append([1])
+        docs.append([int(nn[5]), int(nn[6])]); dws.append([2, 1])
+        docs.append([int(nn[7]), int(nn[8]), int(y)]); dws.append([1, 3, 2])
+    for a_, b_ in zip(dup_src, dup_dst):
+        docs.append([int(b_)]); dws.append([1])
+    docs.append([int(v) for v in dup_dst[:3]]); dws.append([1, 1, 1])
+    doc_off = np.cumsum([0] + [len(v) for v in docs]).astype(np.int64)
+    ids = np.concatenate(docs).astype(np.int32)
+    w = np.concatenate(dws).astype(np.uint32)
+    queries = [[int(y)] for y in qpts] + [[int(y), int(nn[0])] for y, nn in zip(qpts[:8], near[:8])] + \
+              [[int(v)] for v in dup_src[:5]] + [[int(v) for v in dup_src[:3]]]
+    qws = [[1]] * 24 + [[2, 1]] * 8 + [[1]] * 5 + [[1, 1, 1]]
+    q_off = np.cumsum([0] + [len(v) for v in queries]).astype(np.int64)
+    q_ids = np.concatenate(queries).astype(np.int32)
+    q_w = np.concatenate(qws).astype(np.uint32)
+    ix = ft.Index(X, seed=base.tree_seed, max_depth=base.max_depth)
+    ds = ft.Dataset(ix, doc_off, ids, w)
+    got = ds.flowtree(q_off, q_ids, q_w)
+    T = oracle.Tree(X, seed=base.tree_seed, max_depth=base.max_depth)
+
+    def one(qd):
+        qi, di = qd
+        return T.ft(ids[doc_off[di]:doc_off[di + 1]], w[doc_off[di]:doc_off[di + 1]],
+                    q_ids[q_off[qi]:q_off[qi + 1]], q_w[q_off[qi]:q_off[qi + 1]])
+    pairs = [(qi, di) for qi in range(len(queries)) for di in range(len(docs))]
+    ref = np.array(pmap(one, pairs)).reshape(len(queries), len(docs))
+    assert np.sum(ref == 0.0) >= 6                              # duplicate-coordinate pairs are exact zeros
+    assert_ft_close(got.ravel(), ref.ravel(), "near pairs / duplicates")
 
 
 # ---------------------------------------------------------------------------------------------
