@@ -46,16 +46,20 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def tf32_peak_tflops():
+def int8_peak_tops(clocks_held: bool):
+    """Dense int8 tensor peak: the measured bf16 peak (burst when the SM clock held at max during
+    the run, sustained otherwise) x the nominal int8/bf16 ratio 4.5/2.25 (B200_PROFILING.md gives
+    4.5 POPS dense for fp8; B200 sm_100a runs kind::i8 at the same rate)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    ratio = 1.1 / 2.25          # B200_PROFILING.md nominal dense tf32 / bf16
+    ratio = 4.5 / 2.25
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        if "bf16_tflops_sustained" in j:
-            return (float(j["bf16_tflops_sustained"]) * ratio,
-                    "measured bf16 sustained (MEASURED_PEAKS.json) x nominal tf32/bf16 ratio 1.1/2.25")
-    return 1100.0, "fallback (B200_PROFILING.md 1.1 PFLOP/s dense tf32)"
+        key = "bf16_tflops" if clocks_held else "bf16_tflops_sustained"
+        if key in j:
+            return (float(j[key]) * ratio, f"measured bf16 {'burst' if clocks_held else 'sustained'} "
+                                           f"(MEASURED_PEAKS.json {key}) x nominal int8/bf16 ratio 4.5/2.25")
+    return 4500.0, "fallback (B200_PROFILING.md 4.5 POPS dense 8-bit)"
 
 
 class ClockSampler:
@@ -159,6 +163,80 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------------------
+# per-config lines (BASELINE.json configs; the stand-ins for the paper's per-dataset Table 2,
+# PAPER.md:352-364): k-NN batch, Quadtree over all docs, exhaustive Flowtree on a query subset
+FT_SUBSET = {"tiny": 4, "text": 64, "reviews": 64, "image": 16, "stress": 8}
+
+
+def measure_configs(ft, workloads, torch, dev, stream, peak, flush, names):
+    out = {}
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.median(ms)
+
+    for name in names:
+        t0 = time.perf_counter()
+        wl = workloads.make(name)
+        gen_s = time.perf_counter() - t0
+        ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+        ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+        nq, n, k, m = wl.nq, ds.n, wl.k, wl.prefilter_m
+        qi = torch.from_numpy(wl.q_ids).to(dev)
+        qw = torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32)
+        oi = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        ov = torch.empty((nq, k), dtype=torch.float64, device=dev)
+        reps = 2 if name == "image" else 3
+        knn_ms = timed(lambda: ds.knn(wl.q_off, qi, qw, k, m, out_ids=oi, out_val=ov, stream=stream), reps)
+        # Quadtree over all docs for the whole batch (8 B per doc tree node + 16 B per pair)
+        out_qt = torch.empty((nq, n), dtype=torch.float64, device=dev)
+        qt_ms = timed(lambda: ds.quadtree(wl.q_off, qi, qw, out=out_qt, stream=stream), 3)
+        del out_qt
+        qt_bpp = (8 * ds.n_qt + 16 * n) / n
+        # exhaustive Flowtree (FT kernel alone; its distance table timed beside it): 8 B per doc
+        # support point + 16 B per pair
+        nqf = min(nq, FT_SUBSET[name])
+        sub = wl.subset_queries(nqf)
+        si = torch.from_numpy(sub.q_ids).to(dev)
+        sw = torch.from_numpy(sub.q_w.view(np.int32)).to(dev).view(torch.uint32)
+        out_ft = torch.empty((nqf, n), dtype=torch.float64, device=dev)
+        ds.flowtree(sub.q_off, si, sw, out=out_ft, stream=stream)
+        ft.ft_profile_enable(ds.h, True)
+        ft.ft_profile_reset(ds.h)
+        for _ in range(2):
+            flush.zero_()
+            ds.flowtree(sub.q_off, si, sw, out=out_ft, stream=stream)
+        st = ft.profile_dict(ds.h)
+        ft.ft_profile_enable(ds.h, False)
+        del out_ft
+        f_ms, d_ms = st["flowtree"][0] / 2, st["dist_table"][0] / 2
+        ft_bpp = (8 * ds.nnz + 16 * n) / n
+        qt_rate, ft_rate = nq * n / (qt_ms / 1e3), nqf * n / (f_ms / 1e3)
+        out[name] = {
+            "n": n, "N": int(wl.X.shape[0]), "d": int(wl.X.shape[1]), "queries": nq, "k": k, "prefilter_m": m,
+            "knn_ms_per_batch": knn_ms, "knn_queries_per_s": nq / (knn_ms / 1e3),
+            "qt_pairs_per_s": qt_rate, "qt_bytes_per_pair": qt_bpp, "qt_frac_hbm": qt_rate * qt_bpp / 1e9 / peak,
+            "ft_queries": nqf, "ft_pairs_per_s": ft_rate, "ft_bytes_per_pair": ft_bpp,
+            "ft_frac_hbm": ft_rate * ft_bpp / 1e9 / peak, "ft_dist_table_ms": d_ms,
+            "ft_pairs_per_s_incl_table": nqf * n / ((f_ms + d_ms) / 1e3), "gen_s": round(gen_s, 1)}
+        ds.close()
+        ix.close()
+        del wl, qi, qw, oi, ov, si, sw
+        torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
 def run_b200(args):
     import torch
     rank, world, local = dist_info()
@@ -249,7 +327,8 @@ def run_b200(args):
     qt_bytes = Q * (8 * n_qt + 16 * ds.n)
     alg_bytes = {"quadtree": qt_bytes * stages["quadtree"][1], "dist_table": units["dist_table"],
                  "flowtree": units["flowtree"]}
-    kern = {"quadtree": "k_qt (Quadtree estimate, a3)", "dist_table": "k_dist_tc (tcgen05 distance table, a5)",
+    kern = {"quadtree": "k_qt (Quadtree estimate, a3)",
+            "dist_table": "k_dist_i8 (tcgen05 kind::i8 exact distance table, a5)",
             "flowtree": "k_ftd (lane-per-pair Flowtree estimate, a6) + k_flowtree (list mode: pairs sharing an M-node)"}
     traffic_all = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -274,18 +353,26 @@ def run_b200(args):
         rq["note"] = "per-pair algorithmic bytes (record per pair, SURVEY 8(d)); records are read once per 32 queries"
         rq["frac_chunk_amortised"] = rq["frac"] / 32.0
     if "dist_table" in rooflines and units["dist_flops"] > 0:
-        # the distance table is a contraction: its tensor roofline beside the byte one.  TF32 peak =
-        # the measured bf16 sustained peak x the guide's nominal tf32/bf16 ratio (1.1 / 2.25 PF)
-        tf32_peak, tf32_src = tf32_peak_tflops()
+        # the distance table is a contraction on the int8 tensor pipe: its roofline is the tensor one.
+        # Algorithmic ops = 2·rows·s_q·d (one multiply-add per coordinate of every entry);
+        # the exact three-limb kernel executes nine int8 products per algorithmic multiply-add (plus
+        # column padding to 16), reported as "executed" beside it.
+        held = bool(clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"])
+        i8_peak, i8_src = int8_peak_tops(held)
         ms_d, n_d = stages["dist_table"]
         ach_t = units["dist_flops"] / (ms_d / 1e3) / 1e12
-        rooflines["dist_table_tensor"] = {
-            "bound": "tensor", "kernel": kern["dist_table"], "achieved": ach_t, "peak": tf32_peak,
-            "unit": "TFLOP/s", "frac": ach_t / tf32_peak, "traffic": None,
-            "algorithmic_flops_per_launch": units["dist_flops"] / n_d, "launch_ms": ms_d / n_d,
-            "launches": n_d, "peak_source": tf32_src,
-            "note": "algorithmic flops 2*rows*s_q*d; the 3xTF32 kernel issues three MMA products per entry "
-                    "(plus row/column padding), so the tensor pipe executes >= 3x these"}
+        byte_line = rooflines.pop("dist_table")
+        rooflines["dist_table"] = {
+            "bound": "tensor", "kernel": kern["dist_table"], "achieved": ach_t, "peak": i8_peak,
+            "unit": "TOP/s (int8)", "frac": ach_t / i8_peak, "traffic": byte_line["traffic"],
+            "algorithmic_ops_per_launch": units["dist_flops"] / n_d, "launch_ms": ms_d / n_d,
+            "launches": n_d, "share_of_step": ms_d / max(t_ms, 1e-9), "peak_source": i8_src,
+            "executed_int8_ops_per_launch": 9 * units["dist_flops"] / n_d,
+            "frac_executed": 9 * ach_t / i8_peak,
+            "hbm_view": {"achieved_GBps": byte_line["achieved"], "frac": byte_line["frac"],
+                         "algorithmic_bytes_per_launch": byte_line["algorithmic_bytes_per_launch"]},
+            "note": "algorithmic ops 2*rows*s_q*d; exact arithmetic executes 9 int8 limb products per "
+                    "multiply-add (frac_executed is the tensor-pipe share those occupy)"}
     dom = max([s for s in rooflines if s in stages], key=lambda s: stages[s][0])
     roofline = dict(rooflines[dom], dominant_stage=dom)
 
@@ -374,6 +461,12 @@ def run_b200(args):
     e2e = {"value": jobq * args.steps / (e_ms / 1e3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h}
 
+    # ---- every BASELINE.json config on its own (rank 0 at N=1) ----
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = measure_configs(ft, workloads, torch, dev, stream, peak, flush,
+                                  ["tiny", "text", "reviews", "image", "stress"])
+
     # ---- CPU baseline: the oracle, rank 0 at N=1 only, bounded sample ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -399,7 +492,7 @@ def run_b200(args):
                        "qt_records": int(n_qt), "nnz": int(ds.nnz)},
             "ft_estimates_per_s": kernels.get("flowtree_all_docs", {}).get("pairs_per_s"),
             "qt_estimates_per_s": kernels.get("quadtree_all_docs", {}).get("pairs_per_s"),
-            "roofline": roofline, "rooflines_by_stage": rooflines, "kernels": kernels,
+            "roofline": roofline, "rooflines_by_stage": rooflines, "kernels": kernels, "configs": configs,
             "stages_ms_per_step": {s: v[0] / args.steps for s, v in stages.items()},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
             "build_s": build_s, "load_s": load_s,
@@ -421,6 +514,7 @@ def main():
     p.add_argument("--ft-queries", type=int, default=64, help="queries for the exhaustive Flowtree kernel line")
     p.add_argument("--no-kernels", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-configs", action="store_true", help="skip the per-config lines (all five BASELINE configs)")
     p.add_argument("--shard", default="queries", choices=["queries", "docs"],
                    help="multi-GPU layout: replicate docs and split queries (weak), or split docs (strong)")
     args = p.parse_args()

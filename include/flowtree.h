@@ -94,13 +94,21 @@ ft_status ft_dataset_info(const ft_dataset* ds, int64_t* n, int64_t* nnz, int64_
 ft_status ft_quadtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
                                const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
                                void* stream);
-/* Flowtree estimates with the same signature.  The flow is integer exact;
- * distances are FP32 (|rel err| ≲ 1e-6), accumulation FP64; tolerance 1e-5 relative.        */
+/* Flowtree estimates with the same signature.  The flow is integer exact.
+ * Distances: for d ≤ 32 FP32 direct differences; for d > 32 a tensor-core table in exact integer
+ * arithmetic on the points quantised to 24-bit fixed point (unit 2^-e, e the largest exponent with
+ * max|x − mean|·2^e ≤ 2^23 − 2^16): |error| ≤ sqrt(d)·2^-e absolute plus ≈2^-22 relative, and
+ * identical coordinates give exactly 0.  Accumulation FP64 across batches.  Tolerance of the
+ * estimate: 1e-5 relative.  With candidate lists the call reads the per-query
+ * table sizes back once (one stream synchronisation) before the distance stage.               */
 ft_status ft_flowtree_estimate(const ft_dataset* ds, const int64_t* q_off, int32_t nq, const int32_t* q_ids,
                                const uint32_t* q_w, const int64_t* docs, int64_t n_docs, double* out,
                                void* stream);
 /* Parity hook: the Flowtree flow of one (query, doc) pair, HOST outputs, in canonical order
- * (node depth desc, node id asc, src asc, dst asc) — the oracle's emission order.
+ * (node depth desc, node id asc, src asc, dst asc) — the oracle's emission order.  The flow comes
+ * from the kernel that scores the pair in ft_knn / ft_flowtree_estimate: for d > 32 the
+ * lane-per-pair kernel (k_ftd) unless the pair has a matching multi-point cell, else the warp
+ * kernel (k_flowtree).
  *   src = doc vocab id, dst = query vocab id, mass in units of 1/(W·U), node where matched.
  *   FT_ERANGE if more than cap triples (n_out still receives the count).                     */
 ft_status ft_flowtree_flow(const ft_dataset* ds, int32_t q_len, const int32_t* q_ids, const uint32_t* q_w,
@@ -184,7 +192,9 @@ uint64_t ft_launch_count(void);
  *   FT_OPT_QT_WAVES        > 0: CTA waves per SM slot of the Quadtree launch (default 8).
  *   FT_OPT_FTD_CARVEOUT    1..100: k_ftd shared-memory carveout percent (0: sized for 3 CTAs/SM).
  *   FT_OPT_DEBUG           bit mask of diagnostics printed to stderr: 1 distance-table role
- *                          clocks, 2 exact-W1 pivots, 4 selection paths, 8 scratch growth.       */
+ *                          clocks, 2 exact-W1 pivots, 4 selection paths, 8 scratch growth; and
+ *                          16: ft_flowtree_flow fails (FT_ESTATE) unless the lane-per-pair kernel
+ *                          (the one scoring the pair in ft_knn) produced the flow.               */
 typedef enum {
     FT_OPT_VOCAB_HASH = 0,
     FT_OPT_WARP_ONLY = 1,

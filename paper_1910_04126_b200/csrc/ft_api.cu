@@ -213,11 +213,15 @@ ft_status stage_docs(ft_dataset* ds, const int64_t* docs, int64_t n_docs, cudaSt
     return FT_OK;
 }
 
+// the Flowtree stage prices from a distance table (d beyond the on-the-fly limit, within the table
+// kernel's geometry)
+bool ix_uses_table(const ft_index* ix) { return ix->d > FTI_SMALL_D && fti_dist_supported(ix); }
+
 // a5 + a6 over a query batch, chunked so the distance tables stay within a memory budget.
 ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int64_t* d_docs, int64_t docs_ld,
                          int64_t n_docs, double* d_out, int64_t out_ld, cudaStream_t st) {
     const ft_index* ix = ds->ix;
-    if (ix->d <= FTI_SMALL_D || !fti_dist_supported(ix)) {
+    if (!ix_uses_table(ix)) {
         // small d: distances on the fly from shared memory; d beyond the distance-table kernel's
         // shared-memory geometry (> 576): on the fly from global memory (slow, any d)
         StageTimer tm(ds, FTI_ST_FT, st);
@@ -371,8 +375,31 @@ extern "C" ft_status ft_flowtree_flow(const ft_dataset* cds, int32_t q_len, cons
     FTI_RES(ds->s_flowcnt, sizeof(uint32_t));
     FTI_CUDA(cudaMemsetAsync(ds->s_flowcnt.p, 0, sizeof(uint32_t), st));
     FTI_RES(ds->s_vals, sizeof(double));
-    FTI_FT(fti_launch_ft(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{}, ds->s_vals.as<double>(), 1,
-                         ds->s_flow.as<uint32_t>(), ds->s_flowcnt.as<uint32_t>(), fcap, st));
+    // the kernel that scores the pair in the product path exports it: with a distance table
+    // (d > 32) that is the lane-per-pair kernel unless the pair has a matching M-node (or too many
+    // shared ids), which it hands to the warp kernel
+    bool done = false;
+    if (ix_uses_table(ds->ix) && !fti_opt(FT_OPT_WARP_ONLY)) {
+        uint32_t* fl = nullptr;
+        uint32_t* fc = nullptr;
+        const cudaError_t e = fti_launch_ftd(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{},
+                                             ds->s_vals.as<double>(), 1, &fl, &fc, st, ds->s_flow.as<uint32_t>(),
+                                             ds->s_flowcnt.as<uint32_t>(), fcap);
+        if (e != cudaSuccess && e != cudaErrorNotSupported) FTI_CUDA(e);
+        if (e == cudaSuccess) {
+            uint32_t handed = 0;
+            FTI_CUDA(cudaMemcpyAsync(&handed, fc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            FTI_CUDA(cudaStreamSynchronize(st));
+            done = handed == 0;
+        }
+    }
+    if (!done && (fti_opt(FT_OPT_DEBUG) & FTI_DBG_FLOW_FTD))
+        return fti_fail(FT_ESTATE, "ft_flowtree_flow: the pair is not scored by the lane-per-pair kernel");
+    if (!done) {
+        FTI_CUDA(cudaMemsetAsync(ds->s_flowcnt.p, 0, sizeof(uint32_t), st));
+        FTI_FT(fti_launch_ft(ds, S.L, S.qblock, 1, ds->s_docs.as<int64_t>(), 0, 1, FtTable{}, ds->s_vals.as<double>(),
+                             1, ds->s_flow.as<uint32_t>(), ds->s_flowcnt.as<uint32_t>(), fcap, st));
+    }
     uint32_t cnt = 0;
     FTI_CUDA(cudaMemcpyAsync(&cnt, ds->s_flowcnt.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     rc = check_device_errors(ds, st, who);

@@ -13,22 +13,25 @@
 //     exact, so identical coordinates (the same id, or duplicates under distinct ids) give exactly
 //     0 and near pairs suffer no Gram-form cancellation;
 //   * D = sqrt((float)d²)·2^-e in FP32.  |D − ||x − y||| ≤ ||δ_x − δ_y|| ≤ sqrt(d)·2^-e (each
-//     coordinate rounds by ≤ 2^-(e+1)), plus ≈1e-7 relative from the FP32 conversion and sqrt
+//     coordinate rounds by ≤ 2^-(e+1)), plus ≈2^-22 relative from the FP32 conversion and the
+//     MUFU square root
 //     (DESIGN.md §7).
 //
 // k_dist_i8 is persistent (one CTA per SM) and warp specialised over a device-built list of
 // (query, 96-column group, 128-row tile) work items:
-//   * 4 copy warps cp.async the tile's 128 gathered rows, 64 coordinates × 3 limbs (192 B) per K
+//   * 2 copy warps cp.async the tile's 128 gathered rows, 64 coordinates × 3 limbs (192 B) per K
 //     stage, into a 4-deep ring in the canonical no-swizzle K-major core-matrix layout, arriving on
 //     the stage's mbarrier with cp.async.mbarrier.arrive.noinc;
 //   * 1 MMA warp: when the (query, group) changes it bulk-copies the group's pre-arranged B (the
-//     query points' limbs, same layout) into shared memory; per stage an elected lane issues
-//     2 K-steps × 9 products × (1 or 2) 48-column blocks of tcgen05.mma.kind::i8 (M = 128, A and B
-//     from shared memory) into the blocks' TMEM slots (5 tiers × 48 s32 columns each; two slots, so
-//     a one-block item's epilogue overlaps the next item's MMAs) and commits the stage's empty
-//     barrier, then each block's slot-full barrier;
-//   * 8 epilogue warps (2 per TMEM lane quarter, alternating 8-column chunks): tcgen05.ld the five
-//     tiers, combine them exactly in int64, write each row's 8 distances as two 16-byte stores.
+//     query points' limbs, each 48-column block's three limbs stacked along N) into shared memory;
+//     per K step an elected lane issues, per block, three tcgen05.mma.kind::i8 (M = 128,
+//     N = 3·48, A and B from shared memory): A_p·[B_0 | B_1 | B_2] into TMEM columns starting at
+//     p·48, so the product A_p·B_q lands on tier p + q and each A limb is read once per K step (the
+//     first K step splits them so every tier is initialised once).  Accumulators: two TMEM slots
+//     of 5 tiers × 48 s32 columns, so a one-block item's epilogue overlaps the next item's MMAs;
+//   * 8 epilogue warps (2 per TMEM lane quarter, alternating 8-column chunks, the next chunk's
+//     loads in flight): tcgen05.ld the five tiers, combine them exactly in int64 (wide
+//     multiply-adds), write each row's 8 distances as two 16-byte stores.
 // k_tile_plan / k_tiles build the work list, k_dist_prep the per-(query, group) B operand.
 //
 // Candidate vocabulary for the prefiltered pipeline: k_vocab marks every vocab id of the query's
@@ -51,14 +54,15 @@ constexpr int KS = 64;                   // K bytes (= coordinates) per stage an
 constexpr int ROWB = NL * KS;            // global row bytes per stage: [limb][64]
 constexpr int STAGE_LIMB = TM * KS;      // 8 KB
 constexpr int STAGE_BYTES = NL * STAGE_LIMB;
-constexpr int NSTAGE_MAX = 4;
+constexpr int NSTAGE_MAX = 8;
 constexpr int SBO_A = (KS / 16) * 128;   // A stage: bytes between 8-row core-matrix groups
 constexpr int NBLK = 48;                 // accumulator columns per block (5 tiers × 48 = 240 ≤ 256)
 constexpr int NGRP = 2 * NBLK;           // query columns per work item
 constexpr int SLOT_COLS = 256;           // TMEM columns per accumulator slot
-constexpr int NCOPY = 128;               // copy threads (warps 0-3)
-constexpr int MMA_WARP = NCOPY / 32;     // warp 4
-constexpr int NEPI = 8;                  // epilogue warps 5-12
+constexpr int NCOPY = 64;                // copy threads (warps 0-1)
+constexpr int MMA_WARP = NCOPY / 32;     // warp 2
+constexpr int NEPI = 8;                  // epilogue warps 3-10 (11 warps: ≤ 3 per SM sub-partition,
+                                         // so up to 168 registers per thread)
 constexpr int NTHREADS = NCOPY + 32 + 32 * NEPI;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int QMAX_ABS = (1 << 23) - (1 << 16);   // |v| bound: the top balanced limb stays in [−128, 127]
@@ -141,7 +145,7 @@ struct DistArgs {
     long long* ny;              // [nq][ny_ld] Σ v² of the query points
     int ny_ld;
     uint2* qinfo;               // [nq] {B offset / 16 bytes, s_q (0: invalid query)}
-    int4* wdesc;                // [T] {q, tile, g, B offset / 16 of the group}
+    int4* wdesc;                // [T] {q, tile, g | group columns << 16, B offset / 16 of the group}
     int32_t* wrow;              // [T][TM] vocab id of each row of the tile, −1 past the query's rows
     int64_t* tile_base;         // [nq + 1] exclusive prefix of work items per query (T = tile_base[nq])
     const int32_t* rows;        // [nq][rows_cap] or null (row = vocab)
@@ -150,16 +154,30 @@ struct DistArgs {
     const int64_t* row_base;    // [nq] ELEMENT offset of each query's table
     const int32_t* pitch;       // [nq] per-query row pitch (floats)
     float* table;
-    int nstage;                 // A ring depth (2..4, as shared memory allows)
+    int nstage;                 // A ring depth
+    int blk_outer;              // the ring holds a tile's whole K range (nstage == nks)
 };
 
 __device__ unsigned long long g_dbg[16];
+// DBG: clock64 totals of each role's waits (FT_OPT_DEBUG bit 1)
+#define TW(slot, stmt)                                         \
+    do {                                                       \
+        if (DBG) {                                             \
+            const long long t0_ = clock64();                   \
+            stmt;                                              \
+            dbgc[slot] += (unsigned long long)(clock64() - t0_); \
+        } else {                                               \
+            stmt;                                              \
+        }                                                      \
+    } while (0)
 
 template <bool DBG>
-__global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
+__global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, one CTA per SM
     extern __shared__ __align__(1024) uint8_t sm[];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int NSTAGE = a.nstage;
+    unsigned long long dbgc[4] = {0, 0, 0, 0};
+    const long long tstart = DBG ? clock64() : 0;
     // shared memory: A ring [NSTAGE][3 limbs][128 rows × 64 B] | B [3 limbs][≤ 96 rows × kpad] |
     // epilogue ny [96] | barriers
     uint8_t* aring = sm;
@@ -198,33 +216,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
     if (t < NCOPY) {
         // ------------------------------------------------------------------ copy threads
         // lane → (row & 7, 16-byte granule): one cp.async instruction per limb moves 8 rows × 64
-        // contiguous bytes (full sectors); warp cw fills rows 32 cw .. +31 of every stage
+        // contiguous bytes (full sectors); warp cw fills rows 64 cw .. +63 of every stage
+        constexpr int RG = TM / 8 / (NCOPY / 32);   // 8-row groups per copy warp
         const int rl = lane & 7, gq = lane >> 3;
-        uint32_t doff[4];
+        uint32_t doff[RG];
 #pragma unroll
-        for (int rg = 0; rg < 4; rg++) doff[rg] = cm_off(warp * 32 + 8 * rg + rl, 16 * gq, SBO_A);
+        for (int rg = 0; rg < RG; rg++) doff[rg] = cm_off(warp * 8 * RG + 8 * rg + rl, 16 * gq, SBO_A);
         const uint32_t abase = smem_u32(aring);
         const size_t rstride = (size_t)a.nks * ROWB;
-        int32_t px[4];
+        int32_t px[RG];
 #pragma unroll
-        for (int rg = 0; rg < 4; rg++) px[rg] = w_begin < w_end ? a.wrow[w_begin * TM + warp * 32 + 8 * rg + rl] : -1;
+        for (int rg = 0; rg < RG; rg++)
+            px[rg] = w_begin < w_end ? a.wrow[w_begin * TM + warp * 8 * RG + 8 * rg + rl] : -1;
         int s = 0;
         uint32_t eph = 0;
         bool first = true;
         for (int64_t w = w_begin; w < w_end; w++) {
-            const int8_t* src[4];
+            const int8_t* src[RG];
 #pragma unroll
-            for (int rg = 0; rg < 4; rg++) {
+            for (int rg = 0; rg < RG; rg++) {
                 src[rg] = a.Xq + (px[rg] >= 0 ? (int64_t)px[rg] : a.N) * rstride + 16 * gq;
-                if (w + 1 < w_end) px[rg] = a.wrow[(w + 1) * TM + warp * 32 + 8 * rg + rl];
+                if (w + 1 < w_end) px[rg] = a.wrow[(w + 1) * TM + warp * 8 * RG + 8 * rg + rl];
             }
             for (int c = 0; c < a.nks; c++) {
-                if (!first) mbar_wait(&empty[s], eph);
+                if (!first) TW(0, mbar_wait(&empty[s], eph));
                 const uint32_t st = abase + (uint32_t)s * STAGE_BYTES;
 #pragma unroll
                 for (int p = 0; p < NL; p++)
 #pragma unroll
-                    for (int rg = 0; rg < 4; rg++)
+                    for (int rg = 0; rg < RG; rg++)
                         cp_async16(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS);
                 cp_arrive_noinc(&full[s]);
                 if (++s == NSTAGE) {
@@ -244,10 +264,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
         uint32_t fph = 0, bph = 0, dph = 0;
         int64_t kb = 0;            // accumulator blocks issued so far (slot = kb & 1)
         int cur_q = -1, cur_g = -1;
+        int4 ndsc = w_begin < w_end ? a.wdesc[w_begin] : make_int4(0, 0, 0, 0);
         for (int64_t w = w_begin; w < w_end; w++) {
-            const int4 dsc = a.wdesc[w];
-            const int q = dsc.x, g = dsc.z;
-            const int cols = group_cols((int)a.qinfo[q].y, g);
+            const int4 dsc = ndsc;                     // descriptors are loaded one item ahead
+            if (w + 1 < w_end) ndsc = a.wdesc[w + 1];
+            const int q = dsc.x, g = dsc.z & 0xFFFF;
+            const int cols = dsc.z >> 16;
             const int npad = (cols + 15) & ~15;
             const int nb = npad > NBLK ? 2 : 1;
             int nw[2] = {min(npad, NBLK), npad - NBLK};
@@ -256,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
                 if (cur_q >= 0) {
                     if (elect_one()) umma_commit(bdone);
                     __syncwarp();
-                    mbar_wait(bdone, dph);
+                    TW(2, mbar_wait(bdone, dph));
                     dph ^= 1u;
                 }
                 const uint32_t bytes = (uint32_t)NL * npad * a.kpad;
@@ -269,56 +291,91 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
                         : "memory");
                 }
                 __syncwarp();
-                mbar_wait(bfull, bph);
+                TW(2, mbar_wait(bfull, bph));
                 bph ^= 1u;
                 cur_q = q;
                 cur_g = g;
             }
-            const uint32_t blimb = (uint32_t)npad * a.kpad;
-            uint32_t dcol[2];
-            for (int b = 0; b < nb; b++) {
-                const int64_t k = kb + b;
-                const int sl = (int)(k & 1);
-                if (k >= 2) mbar_wait(&acce[sl], (uint32_t)(((k >> 1) - 1) & 1));
-                dcol[b] = tmem + (uint32_t)sl * SLOT_COLS;
-            }
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            for (int c = 0; c < a.nks; c++) {
-                mbar_wait(&full[s], fph);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                if (elect_one()) {
-                    const uint32_t st = abase + (uint32_t)s * STAGE_BYTES;
+            // block b's B region holds its three limbs stacked along N: rows q·nw[b] + j
+            const uint32_t breg[2] = {bbase, bbase + (uint32_t)(3 * nw[0] / 8) * sbo_b};
+            // one block's MMAs over K stages [c0, c1): A_p · [B_0 | B_1 | B_2] (N = 3·nb) into columns
+            // p·nb .. — the product A_p·B_q lands on tier p + q's columns (p + q)·nb, so the nine limb
+            // products take three MMAs and every A limb is read once per K step per block
+            auto issue = [&](int b, uint32_t dcol, int c, uint32_t st) {
+                const uint32_t n = (uint32_t)nw[b];
 #pragma unroll
-                    for (int ks = 0; ks < KS / 32; ks++) {
-                        const uint32_t kbyte = (uint32_t)(c * KS + ks * 32);
-                        for (int b = 0; b < nb; b++) {
-                            const uint32_t idesc = idesc0 | ((uint32_t)(nw[b] >> 3) << 17);
-                            const uint32_t brow = bbase + (uint32_t)(b * (NBLK / 8)) * sbo_b + (kbyte >> 4) * 128;
-#pragma unroll
-                            for (int tt = 0; tt < NTIER; tt++) {
-#pragma unroll
-                                for (int p = (tt > 2 ? tt - 2 : 0); p <= (tt < 2 ? tt : 2); p++) {
-                                    const int qq = tt - p;
-                                    const uint64_t ad = umma_desc(st + p * STAGE_LIMB + ks * 256, SBO_A);
-                                    const uint64_t bd = umma_desc(brow + qq * blimb, sbo_b);
-                                    const uint32_t acc = (c > 0 || ks > 0 || p > (tt > 2 ? tt - 2 : 0)) ? 1u : 0u;
-                                    asm volatile(
-                                        "{\n\t.reg .pred pr;\n\tsetp.ne.b32 pr, %4, 0;\n\t"
-                                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pr;\n\t}" ::"r"(
-                                            dcol[b] + (uint32_t)(tt * NBLK)),
-                                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-                                }
-                            }
-                        }
+                for (int ks = 0; ks < KS / 32; ks++) {
+                    const uint32_t kbyte = (uint32_t)(c * KS + ks * 32);
+                    const uint32_t bk = breg[b] + (kbyte >> 4) * 128;
+                    auto mma = [&](int pl, int q0, int nq, uint32_t acc) {
+                        const uint64_t ad = umma_desc(st + pl * STAGE_LIMB + ks * 256, SBO_A);
+                        const uint64_t bd = umma_desc(bk + (uint32_t)(q0 * n / 8) * sbo_b, sbo_b);
+                        const uint32_t idesc = idesc0 | ((uint32_t)(nq * n >> 3) << 17);
+                        asm volatile(
+                            "{\n\t.reg .pred pr;\n\tsetp.ne.b32 pr, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pr;\n\t}" ::"r"(
+                                dcol + (uint32_t)(pl + q0) * n),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    };
+                    if (c == 0 && ks == 0) {
+                        // first K step: initialise each tier exactly once
+                        mma(0, 0, 3, 0u);              // tiers 0, 1, 2
+                        mma(1, 0, 2, 1u);              // tiers 1, 2
+                        mma(1, 2, 1, 0u);              // tier 3
+                        mma(2, 0, 1, 1u);              // tier 2
+                        mma(2, 1, 1, 1u);              // tier 3
+                        mma(2, 2, 1, 0u);              // tier 4
+                    } else {
+                        mma(0, 0, 3, 1u);
+                        mma(1, 0, 3, 1u);
+                        mma(2, 0, 3, 1u);
                     }
-                    umma_commit(&empty[s]);
                 }
-                __syncwarp();
-                if (++s == NSTAGE) { s = 0; fph ^= 1u; }
-            }
-            for (int b = 0; b < nb; b++) {
-                if (elect_one()) umma_commit(&accf[(int)((kb + b) & 1)]);
-                __syncwarp();
+            };
+            auto acquire = [&](int64_t k) {           // the slot of the k-th block, once drained
+                const int sl = (int)(k & 1);
+                if (k >= 2) TW(1, mbar_wait(&acce[sl], (uint32_t)(((k >> 1) - 1) & 1)));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                return tmem + (uint32_t)sl * SLOT_COLS;
+            };
+            if (a.blk_outer) {
+                // the ring holds the tile's whole K range (stage = K step): block-outer order, so
+                // block 0's accumulator is committed (and drained by the epilogue) while block 1
+                // computes; a stage is released after the last block has read it
+                for (int b = 0; b < nb; b++) {
+                    const uint32_t dcol = acquire(kb + b);
+                    for (int c = 0; c < a.nks; c++) {
+                        if (b == 0) {
+                            TW(0, mbar_wait(&full[c], fph));
+                            asm volatile("tcgen05.fence::after_thread_sync;");
+                        }
+                        if (elect_one()) {
+                            issue(b, dcol, c, abase + (uint32_t)c * STAGE_BYTES);
+                            if (b == nb - 1) umma_commit(&empty[c]);
+                        }
+                        __syncwarp();
+                    }
+                    if (elect_one()) umma_commit(&accf[(int)((kb + b) & 1)]);
+                    __syncwarp();
+                }
+                fph ^= 1u;
+            } else {
+                uint32_t dcol[2];
+                for (int b = 0; b < nb; b++) dcol[b] = acquire(kb + b);
+                for (int c = 0; c < a.nks; c++) {
+                    TW(0, mbar_wait(&full[s], fph));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    if (elect_one()) {
+                        for (int b = 0; b < nb; b++) issue(b, dcol[b], c, abase + (uint32_t)s * STAGE_BYTES);
+                        umma_commit(&empty[s]);
+                    }
+                    __syncwarp();
+                    if (++s == NSTAGE) { s = 0; fph ^= 1u; }
+                }
+                for (int b = 0; b < nb; b++) {
+                    if (elect_one()) umma_commit(&accf[(int)((kb + b) & 1)]);
+                    __syncwarp();
+                }
             }
             kb += nb;
         }
@@ -330,11 +387,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
         const int r = quarter * 32 + lane;            // tile row = TMEM lane
         int64_t kb = 0;
         int cur_q = -1, cur_g = -1;
+        // the next item's descriptor, row id, row norm and table placement, loaded one item ahead
+        int4 ndsc = make_int4(0, 0, 0, 0);
+        int32_t nxid = -1, npitch = 8;
+        long long nnx = 0;
+        int64_t nrb = 0;
+        auto prefetch = [&](int64_t w) {
+            if (w < w_end) {
+                ndsc = a.wdesc[w];
+                nxid = a.wrow[w * TM + r];
+                nnx = nxid >= 0 ? a.xnq[nxid] : 0ll;
+                npitch = a.pitch[ndsc.x];
+                nrb = a.row_base[ndsc.x];
+            }
+        };
+        prefetch(w_begin);
         for (int64_t w = w_begin; w < w_end; w++) {
-            const int4 dsc = a.wdesc[w];
-            const int q = dsc.x, tile = dsc.y, g = dsc.z;
-            const int s_q = (int)a.qinfo[q].y;
-            const int cols = group_cols(s_q, g);
+            const int4 dsc = ndsc;
+            const int32_t xid = nxid;
+            const long long nx = nnx;
+            const int pitch = npitch;
+            const int64_t rbase = nrb;
+            prefetch(w + 1);
+            const int q = dsc.x, tile = dsc.y, g = dsc.z & 0xFFFF;
+            const int cols = dsc.z >> 16;
             const int npad = (cols + 15) & ~15;
             const int nb = npad > NBLK ? 2 : 1;
             if (q != cur_q || g != cur_g) {   // the group's ||ỹ||² (named barrier: epilogue warps only)
@@ -345,43 +421,67 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_dist_i8(DistArgs a) {
                 cur_q = q;
                 cur_g = g;
             }
-            const int32_t xid = a.wrow[w * TM + r];
-            const long long nx = xid >= 0 ? a.xnq[xid] : 0ll;
-            const int pitch = a.pitch[q];
-            float* trow = a.table + a.row_base[q] + ((int64_t)tile * TM + r) * pitch + NGRP * g;
+            float* trow = a.table + rbase + ((int64_t)tile * TM + r) * pitch + NGRP * g;
             for (int b = 0; b < nb; b++, kb++) {
                 const int sl = (int)(kb & 1);
-                mbar_wait(&accf[sl], (uint32_t)((kb >> 1) & 1));
+                TW(0, mbar_wait(&accf[sl], (uint32_t)((kb >> 1) & 1)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)sl * SLOT_COLS;
-                const int nwb = b == 0 ? min(npad, NBLK) : npad - NBLK;
-                for (int c0 = 8 * half; c0 < nwb; c0 += 16) {
-                    int32_t v[NTIER][8];
-                    __syncwarp();
-#pragma unroll
-                    for (int tt = 0; tt < NTIER; tt++) tmem_ld8(tb + (uint32_t)(tt * NBLK + c0), v[tt]);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int nwb = b == 0 ? min(npad, NBLK) : npad - NBLK;   // tier t at columns t·nwb ..
+                // chunks of 8 columns, alternating between the quarter's two warps; the next chunk's
+                // five tier loads are in flight while this chunk is combined (two register sets)
+                const bool rowok = xid >= 0;
+                auto combine = [&](const int32_t (&v)[NTIER][8], int c0) {
                     const int j0 = NBLK * b + c0;            // column within the group
-                    if (xid >= 0 && NGRP * g + j0 < pitch) {
-                        float o[8];
+                    if (!rowok || NGRP * g + j0 >= pitch) return;
+                    float o[8];
 #pragma unroll
-                        for (int u = 0; u < 8; u++) {
-                            // exact: Σ_t 2^{8t} T_t in int64, d² = ||v_x||² + ||v_y||² − 2 v_x·v_y ≥ 0
-                            const long long dot = ((long long)v[4][u] << 32) + ((long long)v[3][u] << 24) +
-                                                  ((long long)v[2][u] << 16) + ((long long)v[1][u] << 8) +
-                                                  (long long)v[0][u];
-                            const long long d2 = nx + eny[j0 + u] - 2ll * dot;
-                            o[u] = __fsqrt_rn((float)d2) * a.scale;
-                        }
-                        *(float4*)(trow + j0) = make_float4(o[0], o[1], o[2], o[3]);
-                        *(float4*)(trow + j0 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                    for (int u = 0; u < 8; u++) {
+                        // exact: d² = ||v_x||² + ||v_y||² − 2 Σ_t 2^{8t} T_t in int64 (wide
+                        // multiply-adds; the 2^33 T4 term only touches the high word), then FP32
+                        long long d2 = nx + eny[j0 + u];
+                        asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[3][u]), "r"(-(1 << 25)));
+                        asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[2][u]), "r"(-(1 << 17)));
+                        asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[1][u]), "r"(-512));
+                        asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[0][u]), "r"(-2));
+                        d2 += (long long)((unsigned long long)(uint32_t)(-2 * v[4][u]) << 32);
+                        float sq;
+                        asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"((float)d2));
+                        o[u] = sq * a.scale;
                     }
+                    *(float4*)(trow + j0) = make_float4(o[0], o[1], o[2], o[3]);
+                    *(float4*)(trow + j0 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                };
+                auto load = [&](int32_t (&v)[NTIER][8], int c0) {
+#pragma unroll
+                    for (int tt = 0; tt < NTIER; tt++) tmem_ld8(tb + (uint32_t)(tt * nwb + c0), v[tt]);
+                };
+                int32_t va[NTIER][8], vb[NTIER][8];
+                int c0 = 8 * half;
+                if (c0 < nwb) load(va, c0);
+                while (c0 < nwb) {
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c0 + 16 < nwb) load(vb, c0 + 16);
+                    combine(va, c0);
+                    if (c0 + 16 >= nwb) break;
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (c0 + 32 < nwb) load(va, c0 + 32);
+                    combine(vb, c0 + 16);
+                    c0 += 32;
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acce[sl]);
             }
         }
+    }
+    if (DBG) {
+        const unsigned long long tt = (unsigned long long)(clock64() - tstart);
+        if (t == 0) { atomicAdd(&g_dbg[0], tt); atomicAdd(&g_dbg[1], dbgc[0]); atomicAdd(&g_dbg[12], 1ull);
+                      atomicAdd(&g_dbg[13], (unsigned long long)(w_end - w_begin)); }
+        if (t == NCOPY) { atomicAdd(&g_dbg[3], tt); atomicAdd(&g_dbg[4], dbgc[0]); atomicAdd(&g_dbg[5], dbgc[1]);
+                          atomicAdd(&g_dbg[6], dbgc[2]); }
+        if (t == NCOPY + 32) { atomicAdd(&g_dbg[7], tt); atomicAdd(&g_dbg[8], dbgc[0]); }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -449,7 +549,8 @@ __global__ void __launch_bounds__(TM) k_tiles(DistArgs a) {
         if (row < nrows) xid = a.rows ? a.rows[(int64_t)q * a.rows_cap + row] : (int32_t)row;
         a.wrow[w * TM + threadIdx.x] = xid;
         if (threadIdx.x == 0)
-            a.wdesc[w] = make_int4(q, (int)tile, (int)g, (int)(qi.x + (uint32_t)g * (NL * a.kpad / 16) * NGRP));
+            a.wdesc[w] = make_int4(q, (int)tile, (int)g | (group_cols((int)qi.y, (int)g) << 16),
+                                   (int)(qi.x + (uint32_t)g * (NL * a.kpad / 16) * NGRP));
     }
 }
 
@@ -473,14 +574,18 @@ __global__ void __launch_bounds__(256) k_dist_prep(DistArgs a) {
     int8_t* bg = a.bq + 16 * (size_t)qi.x + (size_t)g * NL * a.kpad * NGRP;
     const size_t rstride = (size_t)a.nks * ROWB;
     const int sbo_b = a.kpad * 8, gran = a.kpad / 16;
-    // thread per (limb, row, 16-byte K granule)
-    const int total = NL * npad * gran;
+    // block b (columns 48 b ..) stacks its limbs along N: region rows q·nb + j, regions back to back
+    const int nb0 = min(npad, NBLK), nb1 = npad - nb0;
+    const int total = NL * npad * gran;                    // thread per (region row, 16-byte K granule)
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int kg = e % gran, j = (e / gran) % npad, p = e / (gran * npad);
+        const int kg = e % gran, rr = e / gran;            // rr: row over both regions
+        const int b = rr < 3 * nb0 ? 0 : 1;
+        const int rb = b ? rr - 3 * nb0 : rr, nbw = b ? nb1 : nb0;
+        const int p = rb / nbw, j = NBLK * b + rb % nbw;  // limb, query column within the group
         const int64_t src = j < cols ? (int64_t)yid[j] : a.N;     // the zero row pads the group
         const int c = kg / (KS / 16), kb = (kg % (KS / 16)) * 16;
         const uint4 v = *(const uint4*)(a.Xq + src * rstride + (size_t)c * ROWB + p * KS + kb);
-        *(uint4*)(bg + (size_t)p * npad * a.kpad + cm_off(j, 16 * kg, sbo_b)) = v;
+        *(uint4*)(bg + (size_t)(b ? 3 * nb0 : 0) * a.kpad + cm_off(rb, 16 * kg, sbo_b)) = v;
     }
 }
 
@@ -634,7 +739,7 @@ cudaError_t prepare_quantized(ft_index* ix, cudaStream_t st) {
 
 // shared memory the distance-table kernel needs for a ring of `nstage` A stages at d (B resident)
 static size_t dist_smem(int nstage, int kpad) {
-    return (size_t)nstage * STAGE_BYTES + (size_t)NL * NGRP * kpad + NGRP * 8 + 16 * 8 + 64;
+    return (size_t)nstage * STAGE_BYTES + (size_t)NL * NGRP * kpad + NGRP * 8 + (2 * NSTAGE_MAX + 8) * 8 + 64;
 }
 
 bool fti_dist_supported(const ft_index* ix) {
@@ -681,8 +786,15 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.qinfo = ds->s_qinfo.as<uint2>();
     a.wdesc = ds->s_wdesc.as<int4>();
     a.wrow = ds->s_wrow.as<int32_t>();
-    int nstage = NSTAGE_MAX;
-    while (nstage > 2 && dist_smem(nstage, a.kpad) > 227 * 1024) nstage--;
+    // the whole K range of a tile resident (block-outer MMA order) when it fits, else a ring of
+    // 2..4 stages (K-outer order)
+    int nstage = a.nks;
+    a.blk_outer = 1;
+    if (nstage > NSTAGE_MAX || dist_smem(nstage, a.kpad) > 227 * 1024) {
+        a.blk_outer = 0;
+        nstage = 4;
+        while (nstage > 2 && dist_smem(nstage, a.kpad) > 227 * 1024) nstage--;
+    }
     a.nstage = nstage;
     const size_t smem = dist_smem(nstage, a.kpad);
     const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_DIST) != 0;
@@ -695,6 +807,18 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     k_dist_prep<<<dim3((unsigned)nq, (unsigned)G), 256, 0, st>>>(a);
     kern<<<148, NTHREADS, smem, st>>>(a);
     fti_count_launches(4);
+    if (dbg) {
+        unsigned long long h[16];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
+        const double n = h[12] ? (double)h[12] * 1e3 : 1.0;
+        fprintf(stderr, "dist_i8 dbg per CTA (kcyc): copy total %.1f wait_empty %.1f | mma total %.1f wait_full %.1f "
+                        "wait_acce %.1f wait_B %.1f | epi total %.1f wait_accf %.1f | items/CTA %.1f nstage %d\n",
+                h[0] / n, h[1] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n,
+                (double)h[13] / (n / 1e3), a.nstage);
+        memset(h, 0, sizeof(h));
+        cudaMemcpyToSymbol(g_dbg, h, sizeof(h));
+    }
     return cudaGetLastError();
 }
 

@@ -1,24 +1,28 @@
 // ft_flowd.cu — a6 with LANE = PAIR: the Flowtree estimate (§3; greedy flow
 // PAPER.md:495-504) of 32 (query, doc) pairs per warp that share the query.
 //
-// A CTA works for one query: its items and its vocab bitmap + per-word rank (query item index of
-// an id) sit in shared memory; a compact candidate table's row map ({bits, rank} per 32 vocab ids)
-// is read through L2 (staging it cost a CTA per SM: 0.99 vs 0.86 ms per reviews k-NN batch).  Lane l of a warp scores the pair (q, docs[base + l]) on its own:
+// A CTA works for one query over a strided range of candidate positions: the query's items and its
+// vocab bitmap + per-word rank (query item index of an id) sit in shared memory; a compact
+// candidate table's row map ({bits, rank} per 32 vocab ids) is read through L2.  Lane l of a warp
+// scores the pair (q, docs[position l]) on its own:
 //   * M-nodes: a cell with ≥ 2 ground points present on both sides where both keep residual mass
 //     after the leaves' self matches (so phase B of the warp kernel would match there) hands the
 //     pair to the warp kernel (list mode), as do pairs with more than DCAP shared ids;
-//   * self matches (reading R8): one pass over the doc items tests the query bitmap and queues
-//     the shared ids {doc index i, query index j} in increasing vocab order, so both sides of
-//     the merge below consume the queue with a monotone cursor;
+//   * self matches (reading R8): one pass over the doc items tests the query bitmap and queues the
+//     shared ids {doc index i, query index j} in increasing vocab order (sentinels end the queue);
 //   * root: the northwest corner over the residuals in vocab order (reading R10) as a sequential
-//     two-pointer — η = min of the current residuals, the exhausted side advances — with the next
-//     next doc items in a register pipeline (raw records loaded two advances ahead).  The merge
-//     advances in warp-uniform batches of
-//     DRB steps; every lane then issues its DRB table gathers together.
-// All pairs of a CTA read one query's table, so the gathers of a warp hit one L2-resident table
-// (the warp kernel and the lane-per-query kernel spread them over many tables).  Masses are exact
-// u32 (reading R13), distances FP32 from the a5 table, sums FP32 per batch and FP64 across
-// batches — the same triples and the same arithmetic as k_flowtree's root merge.
+//     merge, branch free, one triple per step; the merge advances in warp-uniform batches of DRB
+//     steps, after which every lane issues its DRB table gathers together (software pipelined one
+//     batch deep).  Uniform weights (every doc and query mass 1: the text / reviews / stress
+//     workloads) take a lean step over the two sides' cumulative residual boundaries E, F:
+//     η = min(E, F) − previous boundary, the side(s) whose boundary was reached advance; each item
+//     carries U (doc) or W (query), a shared id's leftover is U − min(U, W) or W − min(U, W); the
+//     doc side reads its shared flag from the query bitmap while the next item is prepared, and
+//     only the query side consumes the queue.
+// All pairs of a CTA read one query's table, so the gathers of a warp hit one L2-resident table.
+// Masses are exact u32 (reading R13), distances FP32 from the a5 table, sums FP32 per batch and FP64
+// across batches.  EXPORT: the flow triples (src, dst, η, node) are written out instead of priced
+// (ft_flowtree_flow's parity hook).
 #include <algorithm>
 
 #include "ft_device.cuh"
@@ -28,19 +32,11 @@ namespace {
 #ifndef FTD_MINB
 #define FTD_MINB 3         // CTAs per SM the register budget allows
 #endif
-#ifndef FTD_DCAP
-#define FTD_DCAP 32
-#endif
 constexpr int DW = 8;      // warps per CTA
-constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
-#ifndef FTD_GMAP
-#define FTD_GMAP 1         // 1: the compact table's row map is read from L2, not staged in shared memory
-#endif
-#ifndef FTD_DRB
-#define FTD_DRB 8
-#endif
-constexpr int DRB = FTD_DRB;   // merge steps per gather batch
-constexpr uint32_t DQ_END = 0xFFFFu;   // queue sentinel: i = j = 255 never matches (s, sq ≤ 255)
+constexpr int DCAP = 32;   // shared ids per pair held in the per-lane queue
+constexpr int DQN = DCAP + 2;            // queue slots per lane: entries + two sentinels
+constexpr int DRB = 8;     // merge steps per gather batch
+constexpr uint32_t DQ_END = 0xFFFFu;     // queue sentinel: i = j = 255 never matches (s, sq ≤ 254)
 
 struct DArgs {
     const uint32_t* doc_off;
@@ -58,8 +54,8 @@ struct DArgs {
     const uint2* map;          // [nq][nw] {bits, rank} rows of the compact table, or null (row = vocab id)
     const int64_t* row_base;   // [nq] ELEMENT offset of each query's table
     const int32_t* pitch;      // [nq] per-query row pitch (floats)
-    int64_t rows_cap;
     int32_t nw, Sq;
+    int unit_w;                // every doc weight is 1
     double* out;
     int64_t out_ld;
     uint32_t* fb_list;
@@ -67,17 +63,37 @@ struct DArgs {
     int64_t fb_cap;
     uint32_t* err;
     unsigned long long* units;
+    // EXPORT: flow triples {src, dst, η, node} and their count; path table for the leaf nodes
+    uint32_t* flow;
+    uint32_t* flowcnt;
+    int32_t flow_cap;
+    const int32_t* path;
+    int32_t cols;
+    const uint8_t* leaf_depth;
 };
 
+template <bool EXPORT>
+__device__ __forceinline__ void ftd_emit(const DArgs& a, uint32_t x, uint32_t y, uint32_t eta, uint32_t node) {
+    if (EXPORT) {
+        const uint32_t idx = atomicAdd(a.flowcnt, 1u);
+        if ((int)idx < a.flow_cap) {
+            a.flow[4 * idx + 0] = x;
+            a.flow[4 * idx + 1] = y;
+            a.flow[4 * idx + 2] = eta;
+            a.flow[4 * idx + 3] = node;
+        }
+    }
+}
+
+template <bool EXPORT>
 __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int q = a.q0 + (int)blockIdx.y;
     const uint8_t* slot = a.qblock + (size_t)q * a.L.stride;
     const QHeader* hdr = (const QHeader*)slot;
-    // shared: qitem[Sq] uint2 | smap[nw] uint2 (compact table, FTD_GMAP=0 only) | qbits[nw] | qrank[nw] | queue[DW][DCAP][32]
+    // shared: qitem[Sq] uint2 | qbits[nw] | qrank[nw] | queue[DW][DQN][32] u16
     uint2* qitem = (uint2*)sm;
-    uint2* smap = qitem + a.Sq;
-    uint32_t* qbits = (uint32_t*)(smap + (a.map && !FTD_GMAP ? a.nw : 0));
+    uint32_t* qbits = (uint32_t*)(qitem + a.Sq);
     uint32_t* qrank = qbits + a.nw;
     uint16_t* queue = (uint16_t*)(qrank + a.nw);
     const uint32_t sq = hdr->s, U = hdr->U, mh_mask = hdr->mh_mask;
@@ -85,42 +101,39 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const uint2* gitems = (const uint2*)(slot + a.L.off_items);
     for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) qitem[i] = gitems[i];
     for (int i = threadIdx.x; i < a.nw; i += blockDim.x) qbits[i] = 0u;
-    if (a.map && !FTD_GMAP) {
-        const uint2* gm = a.map + (int64_t)q * a.nw;
-        for (int i = threadIdx.x; i < a.nw; i += blockDim.x) smap[i] = gm[i];
-    }
     __syncthreads();
+    // bitmap of the query's ids; rank[w] = index of the first query item in word w (items are
+    // sorted by id, so an id's item index is rank[w] + the bits below it).  Only words holding a
+    // query id are ever ranked.
     for (int i = threadIdx.x; i < (int)sq; i += blockDim.x) {
         const uint32_t x = gitems[i].x & FTI_VOCAB_MASK;
         atomicOr(&qbits[x >> 5], 1u << (x & 31));
-    }
-    __syncthreads();
-    {
-        __shared__ int tmp[32];
-        int run = 0;
-        for (int c0 = 0; c0 < a.nw; c0 += blockDim.x) {
-            const int w = c0 + threadIdx.x;
-            const int v = w < a.nw ? __popc(qbits[w]) : 0;
-            int tot;
-            const int r = run + fti_block_exclusive_sum(v, tmp, &tot);
-            if (w < a.nw) qrank[w] = (uint32_t)r;
-            run += tot;
-        }
+        if (i == 0 || ((gitems[i - 1].x & FTI_VOCAB_MASK) >> 5) != (x >> 5)) qrank[x >> 5] = (uint32_t)i;
     }
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint16_t* myq = queue + warp * DCAP * 32 + lane;
-    const float* trow = a.table + a.row_base[q];
-    const uint32_t ld = (uint32_t)a.pitch[q];
+    uint16_t* myq = queue + warp * DQN * 32 + lane;
+    const float* trow = a.table ? a.table + a.row_base[q] : nullptr;
+    const uint32_t ld = a.table ? (uint32_t)a.pitch[q] : 0u;
     const bool smap_on = a.map != nullptr;
     const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
-    (void)gmapq;
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
     const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
     const bool qmn = hdr->n_mn > 0;
+    // uniform weights on both sides (every mass 1): the lean merge
+    const bool uni = a.unit_w && U == sq;
     unsigned ubytes = 0;
     __shared__ unsigned long long skey[DW * 32];
+    // table row offset of vocab id x (compact table: its candidate-vocabulary rank)
+    auto row_off = [&](uint32_t x) -> uint32_t {
+        uint32_t row = x;
+        if (smap_on) {
+            const uint2 mw = __ldg(gmapq + (x >> 5));
+            row = mw.y + __popc(mw.x & ((1u << (x & 31)) - 1u));
+        }
+        return row * ld;
+    };
     const int64_t stride = (int64_t)gridDim.x * DW * 32;
     for (int64_t cbase = (int64_t)blockIdx.x * DW * 32; cbase < a.n_docs; cbase += stride) {
         // the CTA's DW*32 positions sorted by doc support size, so the lanes of a warp run merges
@@ -145,12 +158,13 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
         int64_t doc = -1;
         if (dp < a.n_docs) {
             doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + dp] : dp;
-            outp = a.out + (int64_t)q * a.out_ld + dp;
+            outp = a.out ? a.out + (int64_t)q * a.out_ld + dp : nullptr;
             if (!qok || doc < 0 || doc >= a.n) {
                 // a negative candidate (padding, or a doc another shard owns) scores +inf; an invalid
                 // query or a doc index ≥ n scores NaN (as the warp kernel)
-                *outp = (qok && doc < 0) ? __longlong_as_double(0x7ff0000000000000ll)
-                                         : __longlong_as_double(0x7ff8000000000000ll);
+                if (outp)
+                    *outp = (qok && doc < 0) ? __longlong_as_double(0x7ff0000000000000ll)
+                                             : __longlong_as_double(0x7ff8000000000000ll);
                 if (qok && doc >= a.n) atomicOr(a.err, FTI_ERR_RANGE);
             } else {
                 i0 = a.doc_off[doc];
@@ -159,16 +173,16 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                 active = true;
             }
         }
-        // shared ids, in vocab order: {i | j << 8 | w << 16}
+        // shared ids, in vocab order: {i | j << 8}, then two sentinels
         int nc = 0;
         if (active) {
             for (int i = 0; i < s; i += 8) {
-                uint2 it[8];
+                uint32_t xv[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) it[u] = i + u < s ? a.items[i0 + i + u] : make_uint2(0u, 0u);
+                for (int u = 0; u < 8; u++) xv[u] = i + u < s ? a.items[i0 + i + u].x : 0u;
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
-                    const uint32_t x = it[u].x & FTI_VOCAB_MASK;
+                    const uint32_t x = xv[u] & FTI_VOCAB_MASK;
                     const uint32_t bw = qbits[x >> 5], bm = 1u << (x & 31);
                     if (i + u < s && (bw & bm)) {
                         const uint32_t j = qrank[x >> 5] + __popc(bw & (bm - 1u));
@@ -176,6 +190,10 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                         nc++;
                     }
                 }
+            }
+            if (nc <= DCAP) {
+                myq[nc * 32] = (uint16_t)DQ_END;
+                myq[(nc + 1) * 32] = (uint16_t)DQ_END;
             }
         }
         if (active && nc > DCAP) active = false;
@@ -232,118 +250,207 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
             }
             if (general) active = false;
         }
-        const bool to_list = dp < a.n_docs && outp && !active && s > 0 && qok;
+        const bool to_list = dp < a.n_docs && !active && s > 0 && qok && doc >= 0 && doc < a.n;
         if (to_list) {
             const uint32_t pos = atomicAdd(&a.fb_cnt[q], 1u);
             a.fb_list[(int64_t)q * a.fb_cap + pos] = (uint32_t)dp;
         }
         const bool scored = active;
-        // ---- root northwest corner, lane-sequential, branch-free ----
-        // (ra, ro): residual and table-row offset of doc item i; (ran, ron) item i+1; p2 / p3 the raw
-        // records of items i+2 / i+3 (loaded two advances before use).  rb / rbn: residuals of query
-        // items j / j+1.  ed / eq: the next queued shared id {i | j << 8} for the doc / query side;
-        // eqw the doc weight of eq's item (loaded when eq is set, used at the query side's next hit).
         const uint2* dit = a.items + i0;
         const uint32_t* dw = (const uint32_t*)dit + 1;   // weights, stride 2 words
-        int i = 0, j = 0, cd = 0, cq = 0;
-        uint32_t ed = nc > 0 ? (uint32_t)myq[0] : DQ_END, eq = ed, eqw = 0u;
-        if (nc > 0) eqw = dw[2 * (eq & 0xFFu)];
-        uint32_t ra = 0, ro = 0, ran = 0, ron = 0, rb = 0, rbn = 0;
-        uint2 p2 = make_uint2(0u, 0u), p3 = make_uint2(0u, 0u);
-        // doc item ii from its record it: residual after its self match, and its table-row offset
-        auto doc_prep = [&](const uint2 it, int ii, bool take, uint32_t& r_, uint32_t& o_) {
-            const uint32_t x = it.x & FTI_VOCAB_MASK;
-            uint32_t m = it.y * U;
-            const bool hit = take && (ed & 0xFFu) == (uint32_t)ii;
-            const uint32_t qm = qitem[(ed >> 8) & 0xFFu].y * W;
-            const uint32_t adj = hit ? (qm < m ? qm : m) : 0u;
-            cd += hit;
-            const uint32_t ne = myq[(cd < DCAP ? cd : DCAP - 1) * 32];
-            ed = hit ? (cd < nc ? ne : DQ_END) : ed;
-            uint32_t row = x;
-            if (smap_on) {
-                const uint2 mw = FTD_GMAP ? __ldg(gmapq + (x >> 5)) : smap[x >> 5];
-                row = mw.y + __popc(mw.x & ((1u << (x & 31)) - 1u));
+        if (EXPORT && active) {
+            // the leaves' self matches (singleton leaves: the pair stayed here)
+            for (int c = 0; c < nc; c++) {
+                const uint32_t e = myq[c * 32];
+                const uint32_t x = dit[e & 0xFFu].x & FTI_VOCAB_MASK;
+                const uint32_t dm = dw[2 * (e & 0xFFu)] * U, qm = qitem[e >> 8].y * W;
+                ftd_emit<EXPORT>(a, x, x, dm < qm ? dm : qm, (uint32_t)a.path[(int64_t)x * a.cols + a.leaf_depth[x]]);
             }
-            r_ = m - adj;
-            o_ = row * ld;
-        };
-        // query item jj: residual after its self match
-        auto q_prep = [&](int jj, bool take) {
-            uint32_t m = qitem[jj].y * W;
-            const bool hit = take && ((eq >> 8) & 0xFFu) == (uint32_t)jj;
-            const uint32_t dm = eqw * U;
-            const uint32_t adj = hit ? (dm < m ? dm : m) : 0u;
-            cq += hit;
-            const uint32_t ne = myq[(cq < DCAP ? cq : DCAP - 1) * 32];
-            eq = hit ? (cq < nc ? ne : DQ_END) : eq;
-            if (hit && cq < nc) eqw = dw[2 * (eq & 0xFFu)];
-            return m - adj;
-        };
-        if (active) {
-            const uint2 t0 = dit[0];
-            const uint2 t1 = s > 1 ? dit[1] : t0;
-            if (s > 2) p2 = dit[2];
-            if (s > 3) p3 = dit[3];
-            doc_prep(t0, 0, true, ra, ro);
-            doc_prep(t1, 1, s > 1, ran, ron);
-            rb = q_prep(0, true);
-            rbn = q_prep(sq > 1 ? 1 : 0, sq > 1);
         }
-        const int sqm1 = (int)sq - 1;
         double acc = 0.0;
-        // software pipeline: the gathers of one batch are in flight while the next batch is merged
         float pdv[DRB];
         uint32_t pef[DRB];
 #pragma unroll
         for (int u = 0; u < DRB; u++) { pdv[u] = 0.f; pef[u] = 0u; }
-        while (__any_sync(0xffffffffu, active)) {
-            uint32_t off[DRB];
-            uint32_t ef[DRB];
-#pragma unroll
-            for (int u = 0; u < DRB; u++) {
-                const uint32_t eta = active ? (ra < rb ? ra : rb) : 0u;
-                off[u] = ro + (uint32_t)j;
-                ef[u] = eta;
-                ra -= eta;
-                rb -= eta;
-                const bool ad = active && ra == 0u, aq = active && rb == 0u;
-                // doc side: item i+2 (record p2) becomes the prepared next item
-                uint32_t r2, o2;
-                doc_prep(p2, i + 2, ad && i + 2 < s, r2, o2);
-                ra = ad ? ran : ra;
-                ro = ad ? ron : ro;
-                ran = ad ? r2 : ran;
-                ron = ad ? o2 : ron;
-                p2 = ad ? p3 : p2;
-                if (ad && i + 4 < s) p3 = dit[i + 4];
-                i += ad;
-                // query side: item j+2
-                const int j2 = j + 2 < (int)sq ? j + 2 : sqm1;
-                const uint32_t q2 = q_prep(j2, aq && j + 2 < (int)sq);
-                rb = aq ? rbn : rb;
-                rbn = aq ? q2 : rbn;
-                j += aq;
-                active = active && i < s && j < (int)sq;
+        if (uni) {
+            // ---- root northwest corner, uniform weights ----
+            // E / F: cumulative residual boundary of the current doc item i / query item j; o:
+            // table-row offset of item i; (rn, on): residual and offset of item i+1; x2: vocab id of
+            // item i+2, x3: raw record of item i+3 (read through pn, which may run past the doc's end
+            // into valid records).  A
+            // shared doc item's leftover is U − min(U, W) (its flag comes from the query bitmap); the
+            // query side takes its shared items from the queue (qh = query index of the next one).
+            // Past a side's last item its boundary grows once beyond the total W·U (no overflow:
+            // W·U ≤ 65535²) and never matches again; the merge ends when both sides are done.
+            const uint32_t mm = U < W ? U : W, Ud = U - mm, Wq = W - mm;
+            auto dres = [&](uint32_t x) { return ((qbits[x >> 5] >> (x & 31)) & 1u) ? Ud : U; };
+            int i = 0, j = 0, cq = 0;
+            uint32_t E = 0, F = 0, o = 0, rn = 0, on = 0, x2 = 0, x3 = 0, prev = 0, qh = 0xFFu;
+            uint32_t xc = 0, xn = 0;   // EXPORT: vocab ids of items i, i+1
+            const uint2* pn = dit + 4;
+            if (active) {
+                const uint32_t x0 = dit[0].x & FTI_VOCAB_MASK;
+                const uint32_t x1 = dit[1].x & FTI_VOCAB_MASK;
+                x2 = dit[2].x & FTI_VOCAB_MASK;
+                x3 = dit[3].x;
+                E = dres(x0);
+                o = EXPORT ? 0u : row_off(x0);
+                rn = dres(x1);
+                on = EXPORT ? 0u : row_off(x1);
+                xc = x0;
+                xn = x1;
+                qh = (uint32_t)myq[0] >> 8;
+                const bool h0 = qh == 0u;
+                F = h0 ? Wq : W;
+                if (h0) { cq = 1; qh = (uint32_t)myq[32] >> 8; }
             }
-            float part = 0.f;
+            while (__any_sync(0xffffffffu, active)) {
+                uint32_t off[DRB], ef[DRB];
 #pragma unroll
-            for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
-            acc += (double)part;
+                for (int u = 0; u < DRB; u++) {
+                    const uint32_t cur = E < F ? E : F;
+                    const uint32_t eta = active ? cur - prev : 0u;
+                    off[u] = o + (uint32_t)j;
+                    ef[u] = eta;
+                    if (EXPORT && eta) ftd_emit<EXPORT>(a, xc, qitem[j].x & FTI_VOCAB_MASK, eta, 0u);
+                    prev = cur;
+                    const bool ad = active && E == cur, aq = active && F == cur;
+                    // doc side: item i+1 becomes current, item i+2 is prepared
+                    E = ad ? E + rn : E;
+                    o = ad ? on : o;
+                    const uint32_t r2 = dres(x2), o2 = EXPORT ? 0u : row_off(x2);
+                    rn = ad ? r2 : rn;
+                    on = ad ? o2 : on;
+                    if (EXPORT) { xc = ad ? xn : xc; xn = ad ? x2 : xn; }
+                    // raw records two advances ahead: x3 (item i+3) was loaded one advance ago
+                    if (ad) {
+                        x2 = x3 & FTI_VOCAB_MASK;
+                        x3 = pn->x;
+                    }
+                    pn += ad;
+                    i += ad;
+                    // query side: item j+1 becomes current (queue entries hold j ≤ 253; the sentinel 255)
+                    const bool hq = aq && qh == (uint32_t)(j + 1);
+                    F = aq ? F + (hq ? Wq : W) : F;
+                    const uint32_t ne = (uint32_t)myq[(cq + 1) * 32] >> 8;
+                    qh = hq ? ne : qh;
+                    cq += hq;
+                    j += aq;
+                    active = active && (i < s || j < (int)sq);
+                }
+                if (!EXPORT) {
+                    float part = 0.f;
 #pragma unroll
-            for (int u = 0; u < DRB; u++) {
-                pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
-                pef[u] = ef[u];
+                    for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
+                    acc += (double)part;
+#pragma unroll
+                    for (int u = 0; u < DRB; u++) {
+                        pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
+                        pef[u] = ef[u];
+                    }
+                }
+            }
+        } else {
+            // ---- root northwest corner, general weights, lane-sequential, branch-free ----
+            // (ra, ro): residual and table-row offset of doc item i; (ran, ron) item i+1; p2 / p3 the raw
+            // records of items i+2 / i+3 (loaded two advances before use).  rb / rbn: residuals of query
+            // items j / j+1.  ed / eq: the next queued shared id {i | j << 8} for the doc / query side;
+            // eqw the doc weight of eq's item (loaded when eq is set, used at the query side's next hit).
+            int i = 0, j = 0, cd = 0, cq = 0;
+            uint32_t ed = nc > 0 ? (uint32_t)myq[0] : DQ_END, eq = ed, eqw = 0u;
+            if (nc > 0) eqw = dw[2 * (eq & 0xFFu)];
+            uint32_t ra = 0, ro = 0, ran = 0, ron = 0, rb = 0, rbn = 0, rx = 0, rxn = 0;
+            uint2 p2 = make_uint2(0u, 0u), p3 = make_uint2(0u, 0u);
+            // doc item ii from its record it: residual after its self match, and its table-row offset
+            auto doc_prep = [&](const uint2 it, int ii, bool take, uint32_t& r_, uint32_t& o_, uint32_t& x_) {
+                const uint32_t x = it.x & FTI_VOCAB_MASK;
+                const uint32_t m = it.y * U;
+                const bool hit = take && (ed & 0xFFu) == (uint32_t)ii;
+                const uint32_t qm = qitem[(ed >> 8) & 0xFFu].y * W;
+                const uint32_t adj = hit ? (qm < m ? qm : m) : 0u;
+                cd += hit;
+                const uint32_t ne = myq[cd * 32];
+                ed = hit ? ne : ed;
+                r_ = m - adj;
+                o_ = EXPORT ? 0u : row_off(x);
+                x_ = x;
+            };
+            // query item jj: residual after its self match
+            auto q_prep = [&](int jj, bool take) {
+                const uint32_t m = qitem[jj].y * W;
+                const bool hit = take && ((eq >> 8) & 0xFFu) == (uint32_t)jj;
+                const uint32_t dm = eqw * U;
+                const uint32_t adj = hit ? (dm < m ? dm : m) : 0u;
+                cq += hit;
+                const uint32_t ne = myq[cq * 32];
+                eq = hit ? ne : eq;
+                if (hit && eq != DQ_END) eqw = dw[2 * (eq & 0xFFu)];
+                return m - adj;
+            };
+            if (active) {
+                const uint2 t0 = dit[0];
+                const uint2 t1 = s > 1 ? dit[1] : t0;
+                if (s > 2) p2 = dit[2];
+                if (s > 3) p3 = dit[3];
+                doc_prep(t0, 0, true, ra, ro, rx);
+                doc_prep(t1, 1, s > 1, ran, ron, rxn);
+                rb = q_prep(0, true);
+                rbn = q_prep(sq > 1 ? 1 : 0, sq > 1);
+            }
+            const int sqm1 = (int)sq - 1;
+            while (__any_sync(0xffffffffu, active)) {
+                uint32_t off[DRB];
+                uint32_t ef[DRB];
+#pragma unroll
+                for (int u = 0; u < DRB; u++) {
+                    const uint32_t eta = active ? (ra < rb ? ra : rb) : 0u;
+                    off[u] = ro + (uint32_t)j;
+                    ef[u] = eta;
+                    if (EXPORT && eta) ftd_emit<EXPORT>(a, rx, qitem[j].x & FTI_VOCAB_MASK, eta, 0u);
+                    ra -= eta;
+                    rb -= eta;
+                    const bool ad = active && ra == 0u, aq = active && rb == 0u;
+                    // doc side: item i+2 (record p2) becomes the prepared next item
+                    uint32_t r2, o2, xx2;
+                    doc_prep(p2, i + 2, ad && i + 2 < s, r2, o2, xx2);
+                    ra = ad ? ran : ra;
+                    ro = ad ? ron : ro;
+                    rx = ad ? rxn : rx;
+                    ran = ad ? r2 : ran;
+                    ron = ad ? o2 : ron;
+                    rxn = ad ? xx2 : rxn;
+                    p2 = ad ? p3 : p2;
+                    if (ad && i + 4 < s) p3 = dit[i + 4];
+                    i += ad;
+                    // query side: item j+2
+                    const int j2 = j + 2 < (int)sq ? j + 2 : sqm1;
+                    const uint32_t q2 = q_prep(j2, aq && j + 2 < (int)sq);
+                    rb = aq ? rbn : rb;
+                    rbn = aq ? q2 : rbn;
+                    j += aq;
+                    active = active && i < s && j < (int)sq;
+                }
+                if (!EXPORT) {
+                    float part = 0.f;
+#pragma unroll
+                    for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
+                    acc += (double)part;
+#pragma unroll
+                    for (int u = 0; u < DRB; u++) {
+                        pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
+                        pef[u] = ef[u];
+                    }
+                }
             }
         }
-        {
+        if (!EXPORT) {
             float part = 0.f;
 #pragma unroll
             for (int u = 0; u < DRB; u++) part = fmaf((float)pef[u], pdv[u], part);
             acc += (double)part;
         }
         if (scored) {
-            *outp = acc / (double)((unsigned long long)W * U);
+            if (outp) *outp = EXPORT ? 0.0 : acc / (double)((unsigned long long)W * U);
             ubytes += 8u * (unsigned)s + 16u;
         }
     }
@@ -356,18 +463,21 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
 }  // namespace
 
 // Lane-per-pair Flowtree over n_docs candidate positions per query (d_docs, or all docs when
-// null) with a distance table.  Pairs it cannot score are listed per query in fb_list / fb_cnt
-// (capacity n_docs per query) for the warp kernel's list mode.  cudaErrorNotSupported when the
-// geometry does not fit (supports > 255, N beyond the shared-memory bitmap).
+// null) with a distance table (or, with d_flow, exporting the flow triples instead of pricing).
+// Pairs it cannot score are listed per query in fb_list / fb_cnt (capacity n_docs per query) for
+// the warp kernel's list mode.  cudaErrorNotSupported when the geometry does not fit (supports >
+// 255, N beyond the shared-memory bitmap).
 cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                            const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
-                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st) {
+                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st,
+                           uint32_t* d_flow, uint32_t* d_flowcnt, int32_t flow_cap) {
     const ft_index* ix = ds->ix;
-    if (!tab.table || ds->max_s > 255 || L.smax > 255) return cudaErrorNotSupported;
+    const bool exp = d_flow != nullptr;
+    if ((!tab.table && !exp) || ds->max_s > FTD_MAX_SQ || L.smax > FTD_MAX_SQ) return cudaErrorNotSupported;
     DArgs a{};
     a.nw = (int)((ix->N + 31) / 32);
     a.Sq = std::max(1, L.smax);
-    const size_t smem = 8ull * a.Sq + (tab.map && !FTD_GMAP ? 8ull * a.nw : 0) + 8ull * a.nw + 2ull * DW * DCAP * 32;
+    const size_t smem = 8ull * a.Sq + 8ull * a.nw + 2ull * DW * DQN * 32;
     if (smem > 200 * 1024) return cudaErrorNotSupported;
     cudaError_t e;
     if ((e = ds->s_fblist.reserve((size_t)nq * n_docs * 4)) != cudaSuccess) return e;
@@ -377,45 +487,55 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.mn_off = ds->mn_off; a.mnodes = ds->mnodes; a.mlists = ds->mlists;
     a.qblock = d_qblock; a.L = L;
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;
-    a.table = tab.table; a.map = tab.map; a.row_base = tab.row_base; a.pitch = tab.pitch; a.rows_cap = tab.rows_cap;
+    a.table = exp ? nullptr : tab.table;
+    a.map = exp ? nullptr : tab.map;
+    a.row_base = tab.row_base; a.pitch = tab.pitch;
+    a.unit_w = ds->unit_w ? 1 : 0;
     a.out = d_out; a.out_ld = out_ld;
     a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;
     a.err = ds->err_dev;
-    a.units = ds->units_ptr(FTI_ST_FT);
+    a.units = exp ? nullptr : ds->units_ptr(FTI_ST_FT);
+    a.flow = d_flow; a.flowcnt = d_flowcnt; a.flow_cap = flow_cap;
+    a.path = ix->path; a.cols = ix->d_star + 1; a.leaf_depth = ix->leaf_depth;
+    auto kern = exp ? k_ftd<true> : k_ftd<false>;
     // function attributes are per device; they are set only when they change
     constexpr int MAXDEV = 64;
-    static thread_local int cur_smem[MAXDEV], cur_pct[MAXDEV];
+    static thread_local int cur_smem[2][MAXDEV], cur_pct[2][MAXDEV];
     static thread_local bool init = false;
     if (!init) {
-        for (int i = 0; i < MAXDEV; i++) cur_smem[i] = cur_pct[i] = -1;
+        for (int k = 0; k < 2; k++)
+            for (int i = 0; i < MAXDEV; i++) cur_smem[k][i] = cur_pct[k][i] = -1;
         init = true;
     }
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if (dev >= MAXDEV) return cudaErrorInvalidDevice;
-    if ((int)smem > cur_smem[dev]) {
-        if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    const int ki = exp ? 1 : 0;
+    if ((int)smem > cur_smem[ki][dev]) {
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
-        cur_smem[dev] = (int)smem;
+        cur_smem[ki][dev] = (int)smem;
     }
     // the L1 caches the lanes' doc records between the pre-pass and the merge: give shared memory
-    // only what the target CTAs per SM need (3, or 2 with the 25 KB-class candidate row map)
+    // only what the target CTAs per SM need
     {
-        const int ctas = tab.map && !FTD_GMAP ? 2 : FTD_MINB;
-        const size_t need = (size_t)ctas * (smem + 2176 + 1024);
+        const size_t need = (size_t)FTD_MINB * (smem + 2176 + 1024);
         int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
         if (fti_opt(FT_OPT_FTD_CARVEOUT) > 0) pct = (int)fti_opt(FT_OPT_FTD_CARVEOUT);
         pct = std::min(100, pct);
-        if (pct != cur_pct[dev]) {
-            if ((e = cudaFuncSetAttribute(k_ftd, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess)
+        if (pct != cur_pct[ki][dev]) {
+            if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess)
                 return e;
-            cur_pct[dev] = pct;
+            cur_pct[ki][dev] = pct;
         }
     }
+    // one CTA per 256 positions, x fastest: the resident CTAs then cover one or two queries at a
+    // time, so the table gathers of an exhaustive scan stay in L2 (a strided assignment spreading
+    // the resident CTAs over ~32 queries took 7.7 GB of DRAM instead of 1.4 GB for 64 × 100k pairs)
     const int64_t gx = (n_docs + DW * 32 - 1) / (DW * 32);
     for (int32_t q0 = 0; q0 < nq; q0 += 65535) {
         a.q0 = q0;
-        k_ftd<<<dim3((unsigned)gx, (unsigned)std::min(65535, nq - q0)), DW * 32, smem, st>>>(a);
+        kern<<<dim3((unsigned)gx, (unsigned)std::min(65535, nq - q0)), DW * 32, smem, st>>>(a);
         fti_count_launches(1);
     }
     *fb_list = a.fb_list;

@@ -48,6 +48,7 @@ int64_t fti_opt(int option);
 #define FTI_DBG_EXACT 2
 #define FTI_DBG_SELECT 4
 #define FTI_DBG_ALLOC 8
+#define FTI_DBG_FLOW_FTD 16   // ft_flowtree_flow: fail unless the lane-per-pair kernel produced the flow
 
 // grow-only device buffer
 struct DevBuf {
@@ -136,6 +137,7 @@ struct ft_dataset {
     int64_t n = 0, nnz = 0;
     int32_t max_s = 0;
     int32_t max_mn = 0;        // max M-nodes per doc
+    bool unit_w = false;       // every doc weight is 1
     // Flowtree record: items sorted by vocab id {vocab|flags, w}
     uint32_t* doc_off = nullptr;   // [n+1]
     uint2* items = nullptr;        // [nnz]
@@ -189,10 +191,13 @@ struct FtTable {
 // lane-per-pair Flowtree with a distance table (ft_flowd.cu), candidate lists or all docs; pairs it
 // cannot score are listed per query in *fb_list / *fb_cnt (capacity n_docs per query) for the
 // warp kernel's list mode.  Query supports up to FTD_MAX_SQ.
-#define FTD_MAX_SQ 255
+#define FTD_MAX_SQ 254
+// With d_flow (the parity hook) it writes the pairs' flow triples {src, dst, η, node} instead of
+// pricing them (no table needed).
 cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                            const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, const FtTable& tab, double* d_out,
-                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st);
+                           int64_t out_ld, uint32_t** fb_list, uint32_t** fb_cnt, cudaStream_t st,
+                           uint32_t* d_flow = nullptr, uint32_t* d_flowcnt = nullptr, int32_t flow_cap = 0);
 // exact W1 of per-query candidate lists by the transportation simplex (ft_exact.cu)
 cudaError_t fti_launch_exact(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                              const int64_t* d_docs, int64_t docs_ld, int64_t n_per_q, double* d_out, int64_t out_ld,

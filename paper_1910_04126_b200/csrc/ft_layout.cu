@@ -265,6 +265,8 @@ extern "C" ft_status ft_load_dataset(const ft_index* ix, const int64_t* doc_off,
     ds->n = n;
     ds->nnz = nnz;
     ds->max_s = max_s;
+    ds->unit_w = true;   // every doc weight 1: the lane-per-pair Flowtree kernel's uniform path
+    for (int64_t t = 0; t < nnz && ds->unit_w; t++) ds->unit_w = w[t] == 1u;
     cudaStream_t st;
     FTI_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     std::vector<uint32_t> off32(n + 1);
@@ -333,7 +335,9 @@ extern "C" ft_status ft_load_dataset(const ft_index* ix, const int64_t* doc_off,
     ds->n_mn = tot[1];
     ds->n_ml = tot[2];
     ds->max_mn = (int32_t)hmax;
-    FTI_CUDA(cudaMalloc(&ds->items, sizeof(uint2) * std::max<int64_t>(nnz, 1)));
+    // 8 zero records past the end: the Flowtree kernels prefetch a few items beyond a doc's last
+    FTI_CUDA(cudaMalloc(&ds->items, sizeof(uint2) * (size_t)(nnz + 8)));
+    FTI_CUDA(cudaMemset(ds->items + nnz, 0, sizeof(uint2) * 8));
     FTI_CUDA(cudaMalloc(&ds->W, sizeof(uint32_t) * n));
     FTI_CUDA(cudaMalloc(&ds->A, sizeof(unsigned long long) * n));
     FTI_CUDA(cudaMalloc(&ds->qt, sizeof(uint2) * std::max<int64_t>(ds->n_qt, 1)));

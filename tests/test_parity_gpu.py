@@ -268,6 +268,38 @@ def test_lane_per_pair_flowtree_matches_other_kernels(ft, opt, name, nq, mode):
     assert np.array_equal(a == 0.0, b == 0.0)
 
 
+@pytest.mark.parametrize("name", ["reviews", "stress", "text"])
+def test_flow_export_lane_per_pair_kernel_bit_exact(ft, opt, name):
+    """The flow of the kernel that scores the d = 300 pairs (k_ftd, lane per pair) exported triple by
+    triple and compared bit-exact with the oracle's greedy flow (readings R8, R10):
+    self matches at the leaves and the root's northwest corner.  FT_OPT_DEBUG bit 16 makes
+    ft_flowtree_flow fail unless k_ftd produced the flow; the few pairs it hands to the warp kernel
+    (a matching multi-point cell) are checked through the warp kernel instead."""
+    wl = get_workload(name, n_docs=3000, n_queries=6)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    rng = np.random.default_rng(7)
+    n_ftd = n_warp = n_self = 0
+    for q in range(wl.nq):
+        b, bw = wl.query(q)
+        for d in rng.choice(wl.n, 25, replace=False):
+            o = T.flow(*wl.doc(int(d)), b, bw)
+            ft.ft_set_option(ft.FT_OPT_DEBUG, 16)
+            try:
+                g = ds.flow(b, bw, int(d))
+                n_ftd += 1
+            except ft.FlowtreeError as e:
+                assert e.status == ft.FT_ESTATE, e
+                ft.ft_set_option(ft.FT_OPT_DEBUG, 0)
+                g = ds.flow(b, bw, int(d))
+                n_warp += 1
+            for key in ("src", "dst", "mass", "node"):
+                assert np.array_equal(g[key], o[key].astype(g[key].dtype)), (q, int(d), key)
+            n_self += int(np.sum(o["node"] != 0))
+    assert n_ftd >= 0.9 * (n_ftd + n_warp), (n_ftd, n_warp)
+    assert n_self > 0                                  # leaf self matches were exercised
+
+
 @pytest.mark.parametrize("big", [False, True])
 def test_flowtree_degenerate_and_maximum_supports(ft, big):
     """Supports at the edges of the lane-per-pair kernel's geometry, through the distance table

@@ -3,7 +3,7 @@
 # Each ncu command runs only after the same command line exited 0 without ncu.
 set -u
 mkdir -p gpurun_out
-B="python bench.py --steps 2 --warmup 3 --no-kernels --no-cpu-baseline"
+B="python bench.py --steps 2 --warmup 3 --no-kernels --no-cpu-baseline --no-configs"
 $B > gpurun_out/bench_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B \
   > gpurun_out/ncu_launches.log 2>&1
