@@ -85,7 +85,8 @@ __device__ __forceinline__ void ftd_emit(const DArgs& a, uint32_t x, uint32_t y,
     }
 }
 
-template <bool EXPORT>
+// MAP: the table is compact (rows = the candidates' vocabulary, looked up in the row map)
+template <bool EXPORT, bool MAP>
 __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int q = a.q0 + (int)blockIdx.y;
@@ -116,7 +117,6 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     uint16_t* myq = queue + warp * DQN * 32 + lane;
     const float* trow = a.table ? a.table + a.row_base[q] : nullptr;
     const uint32_t ld = a.table ? (uint32_t)a.pitch[q] : 0u;
-    const bool smap_on = a.map != nullptr;
     const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
     const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     // table row offset of vocab id x (compact table: its candidate-vocabulary rank)
     auto row_off = [&](uint32_t x) -> uint32_t {
         uint32_t row = x;
-        if (smap_on) {
+        if (MAP) {
             const uint2 mw = __ldg(gmapq + (x >> 5));
             row = mw.y + __popc(mw.x & ((1u << (x & 31)) - 1u));
         }
@@ -284,8 +284,9 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
             // W·U ≤ 65535²) and never matches again; the merge ends when both sides are done.
             const uint32_t mm = U < W ? U : W, Ud = U - mm, Wq = W - mm;
             auto dres = [&](uint32_t x) { return ((qbits[x >> 5] >> (x & 31)) & 1u) ? Ud : U; };
-            int i = 0, j = 0, cq = 0;
+            int i = 0, j = 0;
             uint32_t E = 0, F = 0, o = 0, rn = 0, on = 0, x2 = 0, x3 = 0, prev = 0, qh = 0xFFu;
+            uint32_t qaddr = (uint32_t)__cvta_generic_to_shared(myq);   // queue head (64 B per entry)
             uint32_t xc = 0, xn = 0;   // EXPORT: vocab ids of items i, i+1
             const uint2* pn = dit + 4;
             if (active) {
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                 qh = (uint32_t)myq[0] >> 8;
                 const bool h0 = qh == 0u;
                 F = h0 ? Wq : W;
-                if (h0) { cq = 1; qh = (uint32_t)myq[32] >> 8; }
+                if (h0) { qaddr += 64u; qh = (uint32_t)myq[32] >> 8; }
             }
             while (__any_sync(0xffffffffu, active)) {
                 uint32_t off[DRB], ef[DRB];
@@ -332,9 +333,10 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     // query side: item j+1 becomes current (queue entries hold j ≤ 253; the sentinel 255)
                     const bool hq = aq && qh == (uint32_t)(j + 1);
                     F = aq ? F + (hq ? Wq : W) : F;
-                    const uint32_t ne = (uint32_t)myq[(cq + 1) * 32] >> 8;
-                    qh = hq ? ne : qh;
-                    cq += hq;
+                    uint32_t ne;
+                    asm("ld.shared.u16 %0, [%1];" : "=r"(ne) : "r"(qaddr + 64u));
+                    qh = hq ? ne >> 8 : qh;
+                    qaddr += hq ? 64u : 0u;
                     j += aq;
                     active = active && (i < s || j < (int)sq);
                 }
@@ -497,20 +499,20 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.units = exp ? nullptr : ds->units_ptr(FTI_ST_FT);
     a.flow = d_flow; a.flowcnt = d_flowcnt; a.flow_cap = flow_cap;
     a.path = ix->path; a.cols = ix->d_star + 1; a.leaf_depth = ix->leaf_depth;
-    auto kern = exp ? k_ftd<true> : k_ftd<false>;
+    auto kern = exp ? k_ftd<true, false> : (a.map ? k_ftd<false, true> : k_ftd<false, false>);
     // function attributes are per device; they are set only when they change
     constexpr int MAXDEV = 64;
-    static thread_local int cur_smem[2][MAXDEV], cur_pct[2][MAXDEV];
+    static thread_local int cur_smem[3][MAXDEV], cur_pct[3][MAXDEV];
     static thread_local bool init = false;
     if (!init) {
-        for (int k = 0; k < 2; k++)
+        for (int k = 0; k < 3; k++)
             for (int i = 0; i < MAXDEV; i++) cur_smem[k][i] = cur_pct[k][i] = -1;
         init = true;
     }
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if (dev >= MAXDEV) return cudaErrorInvalidDevice;
-    const int ki = exp ? 1 : 0;
+    const int ki = exp ? 2 : (a.map ? 1 : 0);
     if ((int)smem > cur_smem[ki][dev]) {
         if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return e;
