@@ -1,8 +1,9 @@
 """Build the in-tree CUDA library ``libflowtree_b200.so`` for sm_100a with nvcc.
 
-Usage: ``python -m paper_1910_04126_b200.build [--force]``.  Objects are compiled in parallel
-into ``build/`` and linked (static cudart) next to this file, so the ``.so`` travels with the
-repository snapshot to the GPU box.
+Usage: ``python -m paper_1910_04126_b200.build [--force] [--checked]``.  Objects are compiled in
+parallel into ``build/`` and linked (static cudart) next to this file, so the ``.so`` travels with
+the repository snapshot to the GPU box.  ``--checked`` builds ``libflowtree_b200_checked.so`` with
+device-side bounds assertions (FTI_CHECKED; select it with FT_LIB for a test run).
 """
 from __future__ import annotations
 
@@ -17,6 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libflowtree_b200.so")
+OBJ_CHECKED = os.path.join(ROOT, "build", "obj_checked")
+LIB_CHECKED = os.path.join(HERE, "libflowtree_b200_checked.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -38,39 +41,40 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src, checked=False):
+    obj = os.path.join(OBJ_CHECKED if checked else OBJ, os.path.basename(src)[:-3] + ".o")
     if not _stale(obj, [src] + _headers()):
         return obj, ""
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + (["-DFTI_CHECKED=1"] if checked else []) + ["-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{p.stderr}")
     return obj, p.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    obj_dir, lib = (OBJ_CHECKED, LIB_CHECKED) if checked else (OBJ, LIB)
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = _sources()
     if force:
-        for o in glob.glob(os.path.join(OBJ, "*.o")):
+        for o in glob.glob(os.path.join(obj_dir, "*.o")):
             os.remove(o)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(lambda s_: _compile(s_, checked), srcs))
     objs = [r[0] for r in results]
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if force or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    if force or _stale(lib, objs):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{p.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

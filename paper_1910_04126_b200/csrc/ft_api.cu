@@ -240,7 +240,9 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     size_t budget = ds->table_budget;
     if (fti_opt(FT_OPT_TABLE_BUDGET_MB) > 0) budget = (size_t)fti_opt(FT_OPT_TABLE_BUDGET_MB) << 20;
     const int64_t qcap = fti_opt(FT_OPT_TABLE_CHUNK) > 0 ? fti_opt(FT_OPT_TABLE_CHUNK) : (int64_t)nq;
-    // per query: table rows, pitch (floats) and ELEMENT offset within its chunk.  With candidate
+    // per query: table rows, row pitch (floats) and ELEMENT offset within its chunk.  (A
+    // column-major table — the distance kernel's lanes storing whole 128-byte column segments —
+    // was measured: distance table 4.46 → 4.82 ms, Flowtree 0.75 → 0.68 ms; not kept.)  With candidate
     // lists the rows are the candidates' vocabulary (compact, counted on the device by k_vocab and
     // read back once: the tables are then sized exactly); exhaustively every vocab id is a row.
     const bool use_map = d_docs != nullptr;
@@ -265,6 +267,8 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
     for (int32_t q = 0; q < nq; q++) {
         const int64_t s = S.qoff_host[q + 1] - S.qoff_host[q];
         pitch[q] = (int32_t)((s + 7) & ~7);          // 32-byte rows
+        if ((uint64_t)rowcnt[q] * (uint64_t)pitch[q] >= (1ull << 32))
+            return fti_fail(FT_ERANGE, "Flowtree: a query's distance table exceeds 2^32 entries (N x support)");
         const size_t bytes = (size_t)rowcnt[q] * (size_t)pitch[q] * 4;
         if (q == 0 || in_chunk >= qcap || (cur > 0 && cur + bytes > budget)) {
             chunk_q0.push_back(q);
@@ -293,7 +297,10 @@ ft_status flowtree_stage(ft_dataset* ds, const Staged& S, int32_t nq, const int6
         tab.rows_cap = rows_cap;
         tab.row_base = ds->s_rowbase.as<int64_t>() + q0;
         tab.pitch = ds->s_pitch.as<int32_t>() + q0;
-        if (use_map) tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
+        if (use_map) {
+            tab.map = ds->s_map.as<uint2>() + (int64_t)q0 * nwords;
+            tab.rowcnt = rowcnt_c;
+        }
         {
             StageTimer tm(ds, FTI_ST_DIST, st);
             FTI_CUDA(fti_launch_dist_table(ds, S.L, qb, nqc, rows_c, rowcnt_c, rows_cap, tab.row_base, tab.pitch,

@@ -59,7 +59,13 @@ constexpr int SBO_A = (KS / 16) * 128;   // A stage: bytes between 8-row core-ma
 constexpr int NBLK = 48;                 // accumulator columns per block (5 tiers × 48 = 240 ≤ 256)
 constexpr int NGRP = 2 * NBLK;           // query columns per work item
 constexpr int SLOT_COLS = 256;           // TMEM columns per accumulator slot
-constexpr int NCOPY = 64;                // copy threads (warps 0-1)
+#ifndef FTD_NCOPY
+#define FTD_NCOPY 64
+#endif
+#ifndef FTD_EPI_DB
+#define FTD_EPI_DB 1                     // epilogue: next chunk's tier loads in flight (two register sets)
+#endif
+constexpr int NCOPY = FTD_NCOPY;         // copy threads (warps 0 .. NCOPY/32 − 1)
 constexpr int MMA_WARP = NCOPY / 32;     // warp 2
 constexpr int NEPI = 8;                  // epilogue warps 3-10 (11 warps: ≤ 3 per SM sub-partition,
                                          // so up to 168 registers per thread)
@@ -105,8 +111,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     }
 }
+#ifndef FTD_L2POL
+#define FTD_L2POL 0        // 1: X̃q rows evict_last, table stores evict_first in L2
+#endif
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_pol(uint32_t dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_f1(float* p, float v, uint64_t pol) {
+    if (FTD_L2POL)
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+    else
+        *p = v;
+}
+__device__ __forceinline__ void st_f4(float* p, float4 v, uint64_t pol) {
+    if (FTD_L2POL)
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+                     "f"(v.z), "f"(v.w), "l"(pol)
+                     : "memory");
+    else
+        *(float4*)p = v;
 }
 // arrive on `bar` once all of this thread's prior cp.async copies have landed (count not incremented)
 __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
@@ -120,6 +157,17 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t* v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(taddr));
+}
+
+// FP32 value of a non-negative integer < 2^57 (relative error < 2^-23) on the FMA/ALU pipes: three
+// 23-bit chunks, each converted exactly by the 2^23 magic-number add.  (I2F.S64 runs on the XU pipe,
+// which the epilogue's conversions had saturated — 97% XU, ncu.)
+__device__ __forceinline__ float u57_to_f32(unsigned long long u) {
+    const uint32_t c0 = (uint32_t)u & 0x7FFFFFu, c1 = (uint32_t)(u >> 23) & 0x7FFFFFu, c2 = (uint32_t)(u >> 46);
+    const float f0 = __int_as_float(0x4B000000 | c0) - 8388608.f;
+    const float f1 = __int_as_float(0x4B000000 | c1) - 8388608.f;
+    const float f2 = __int_as_float(0x4B000000 | c2) - 8388608.f;
+    return fmaf(f2, 70368744177664.f, fmaf(f1, 8388608.f, f0));   // f2·2^46 + f1·2^23 + f0
 }
 
 // byte offset of (row r, K byte kb) in a K-major no-swizzle core-matrix tile whose 8-row groups are
@@ -172,7 +220,13 @@ __device__ unsigned long long g_dbg[16];
     } while (0)
 
 template <bool DBG>
-__global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, one CTA per SM
+// NTHREADS threads, one CTA per SM; ≤ 3 warps per SM sub-partition leave 168 registers a thread
+#if (FTD_NCOPY / 32 + 1 + 8) <= 12
+#define FTD_KATTR __maxnreg__(168)
+#else
+#define FTD_KATTR __launch_bounds__(NTHREADS, 1)
+#endif
+__global__ void FTD_KATTR k_dist_i8(DistArgs a) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int NSTAGE = a.nstage;
@@ -217,26 +271,28 @@ __global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, 
         // ------------------------------------------------------------------ copy threads
         // lane → (row & 7, 16-byte granule): one cp.async instruction per limb moves 8 rows × 64
         // contiguous bytes (full sectors); warp cw fills rows 64 cw .. +63 of every stage
-        constexpr int RG = TM / 8 / (NCOPY / 32);   // 8-row groups per copy warp
+        constexpr int NCW = NCOPY / 32, RG = (TM / 8 + NCW - 1) / NCW;   // 8-row groups per copy warp
         const int rl = lane & 7, gq = lane >> 3;
         uint32_t doff[RG];
 #pragma unroll
-        for (int rg = 0; rg < RG; rg++) doff[rg] = cm_off(warp * 8 * RG + 8 * rg + rl, 16 * gq, SBO_A);
+        for (int rg = 0; rg < RG; rg++) doff[rg] = cm_off((warp + NCW * rg) * 8 + rl, 16 * gq, SBO_A);
         const uint32_t abase = smem_u32(aring);
         const size_t rstride = (size_t)a.nks * ROWB;
+        auto grp_ok = [&](int rg) { return warp + NCW * rg < TM / 8; };
         int32_t px[RG];
 #pragma unroll
         for (int rg = 0; rg < RG; rg++)
-            px[rg] = w_begin < w_end ? a.wrow[w_begin * TM + warp * 8 * RG + 8 * rg + rl] : -1;
+            px[rg] = (w_begin < w_end && grp_ok(rg)) ? a.wrow[w_begin * TM + (warp + NCW * rg) * 8 + rl] : -1;
         int s = 0;
         uint32_t eph = 0;
         bool first = true;
+        const uint64_t pol = FTD_L2POL ? l2_policy_last() : 0ull;
         for (int64_t w = w_begin; w < w_end; w++) {
             const int8_t* src[RG];
 #pragma unroll
             for (int rg = 0; rg < RG; rg++) {
                 src[rg] = a.Xq + (px[rg] >= 0 ? (int64_t)px[rg] : a.N) * rstride + 16 * gq;
-                if (w + 1 < w_end) px[rg] = a.wrow[(w + 1) * TM + warp * 8 * RG + 8 * rg + rl];
+                if (w + 1 < w_end && grp_ok(rg)) px[rg] = a.wrow[(w + 1) * TM + (warp + NCW * rg) * 8 + rl];
             }
             for (int c = 0; c < a.nks; c++) {
                 if (!first) TW(0, mbar_wait(&empty[s], eph));
@@ -245,7 +301,10 @@ __global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, 
                 for (int p = 0; p < NL; p++)
 #pragma unroll
                     for (int rg = 0; rg < RG; rg++)
-                        cp_async16(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS);
+                        if (grp_ok(rg)) {
+                            if (FTD_L2POL) cp_async16_pol(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS, pol);
+                            else cp_async16(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS);
+                        }
                 cp_arrive_noinc(&full[s]);
                 if (++s == NSTAGE) {
                     s = 0;
@@ -387,6 +446,7 @@ __global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, 
         const int r = quarter * 32 + lane;            // tile row = TMEM lane
         int64_t kb = 0;
         int cur_q = -1, cur_g = -1;
+        const uint64_t wpol = FTD_L2POL ? l2_policy_first() : 0ull;
         // the next item's descriptor, row id, row norm and table placement, loaded one item ahead
         int4 ndsc = make_int4(0, 0, 0, 0);
         int32_t nxid = -1, npitch = 8;
@@ -424,51 +484,70 @@ __global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, 
             float* trow = a.table + rbase + ((int64_t)tile * TM + r) * pitch + NGRP * g;
             for (int b = 0; b < nb; b++, kb++) {
                 const int sl = (int)(kb & 1);
+                const int nwb = b == 0 ? min(npad, NBLK) : npad - NBLK;   // tier t at columns t·nwb ..
+                // ||ỹ||² of this warp's columns, one per lane (lane l: chunk l >> 3, column l & 7),
+                // read before the wait and broadcast by shuffles: shared-memory loads in the combine
+                // queued behind the tensor core's operand reads (ncu: ≈40% of the combine time)
+                long long nyl = 0;
+                {
+                    const int cidx = 8 * half + 16 * (lane >> 3) + (lane & 7);
+                    if (cidx < nwb) nyl = eny[NBLK * b + cidx];
+                }
                 TW(0, mbar_wait(&accf[sl], (uint32_t)((kb >> 1) & 1)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)sl * SLOT_COLS;
-                const int nwb = b == 0 ? min(npad, NBLK) : npad - NBLK;   // tier t at columns t·nwb ..
                 // chunks of 8 columns, alternating between the quarter's two warps; the next chunk's
                 // five tier loads are in flight while this chunk is combined (two register sets)
                 const bool rowok = xid >= 0;
                 auto combine = [&](const int32_t (&v)[NTIER][8], int c0) {
                     const int j0 = NBLK * b + c0;            // column within the group
-                    if (!rowok || NGRP * g + j0 >= pitch) return;
+                    const int kc = (c0 - 8 * half) >> 4;     // this warp's chunk index (0..2)
                     float o[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
                         // exact: d² = ||v_x||² + ||v_y||² − 2 Σ_t 2^{8t} T_t in int64 (wide
                         // multiply-adds; the 2^33 T4 term only touches the high word), then FP32
-                        long long d2 = nx + eny[j0 + u];
+                        long long d2 = nx + __shfl_sync(0xffffffffu, nyl, 8 * kc + u);
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[3][u]), "r"(-(1 << 25)));
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[2][u]), "r"(-(1 << 17)));
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[1][u]), "r"(-512));
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[0][u]), "r"(-2));
                         d2 += (long long)((unsigned long long)(uint32_t)(-2 * v[4][u]) << 32);
                         float sq;
-                        asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"((float)d2));
+                        asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(u57_to_f32((unsigned long long)d2)));
                         o[u] = sq * a.scale;
                     }
-                    *(float4*)(trow + j0) = make_float4(o[0], o[1], o[2], o[3]);
-                    *(float4*)(trow + j0 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+                    if (!rowok || NGRP * g + j0 >= pitch) return;
+                    FTI_ASSERT(NGRP * g + j0 + 8 <= pitch && (!a.rowcnt || (int64_t)tile * TM + r < a.rowcnt[q]));
+                    st_f4(trow + j0, make_float4(o[0], o[1], o[2], o[3]), wpol);
+                    st_f4(trow + j0 + 4, make_float4(o[4], o[5], o[6], o[7]), wpol);
                 };
                 auto load = [&](int32_t (&v)[NTIER][8], int c0) {
 #pragma unroll
                     for (int tt = 0; tt < NTIER; tt++) tmem_ld8(tb + (uint32_t)(tt * nwb + c0), v[tt]);
                 };
+#if FTD_EPI_DB
                 int32_t va[NTIER][8], vb[NTIER][8];
                 int c0 = 8 * half;
                 if (c0 < nwb) load(va, c0);
                 while (c0 < nwb) {
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
                     if (c0 + 16 < nwb) load(vb, c0 + 16);
-                    combine(va, c0);
+                    TW(2, combine(va, c0));
                     if (c0 + 16 >= nwb) break;
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
                     if (c0 + 32 < nwb) load(va, c0 + 32);
-                    combine(vb, c0 + 16);
+                    TW(2, combine(vb, c0 + 16));
                     c0 += 32;
                 }
+#else
+                for (int c0 = 8 * half; c0 < nwb; c0 += 16) {
+                    int32_t va[NTIER][8];
+                    load(va, c0);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    combine(va, c0);
+                }
+#endif
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acce[sl]);
@@ -481,7 +560,8 @@ __global__ void __maxnreg__(168) k_dist_i8(DistArgs a) {   // NTHREADS threads, 
                       atomicAdd(&g_dbg[13], (unsigned long long)(w_end - w_begin)); }
         if (t == NCOPY) { atomicAdd(&g_dbg[3], tt); atomicAdd(&g_dbg[4], dbgc[0]); atomicAdd(&g_dbg[5], dbgc[1]);
                           atomicAdd(&g_dbg[6], dbgc[2]); }
-        if (t == NCOPY + 32) { atomicAdd(&g_dbg[7], tt); atomicAdd(&g_dbg[8], dbgc[0]); }
+        if (t == NCOPY + 32) { atomicAdd(&g_dbg[7], tt); atomicAdd(&g_dbg[8], dbgc[0]); atomicAdd(&g_dbg[9], dbgc[1]);
+                               atomicAdd(&g_dbg[10], dbgc[2]); }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -813,8 +893,9 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
         cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
         const double n = h[12] ? (double)h[12] * 1e3 : 1.0;
         fprintf(stderr, "dist_i8 dbg per CTA (kcyc): copy total %.1f wait_empty %.1f | mma total %.1f wait_full %.1f "
-                        "wait_acce %.1f wait_B %.1f | epi total %.1f wait_accf %.1f | items/CTA %.1f nstage %d\n",
-                h[0] / n, h[1] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n,
+                        "wait_acce %.1f wait_B %.1f | epi total %.1f wait_accf %.1f tmem_wait %.1f combine %.1f | "
+                        "items/CTA %.1f nstage %d\n",
+                h[0] / n, h[1] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n, h[9] / n, h[10] / n,
                 (double)h[13] / (n / 1e3), a.nstage);
         memset(h, 0, sizeof(h));
         cudaMemcpyToSymbol(g_dbg, h, sizeof(h));

@@ -90,6 +90,7 @@ __device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_
             const uint2 m = c.map[x >> 5];
             row = (int64_t)(m.y + __popc(m.x & ((1u << (x & 31)) - 1u)));
         }
+        FTI_ASSERT(jq < (int)c.tld && (!c.a->tab.rowcnt || row < c.a->tab.rowcnt[c.q]));
         return c.trow_base[row * c.tld + jq];
     }
     // on the fly, FP32 direct differences (the query row from shared memory when staged)
@@ -270,7 +271,10 @@ __device__ void root_merge(const PairCtx& c, int la, int lb, int lane, double& c
                 }
                 float dv[RB];
 #pragma unroll
-                for (int u = 0; u < RB; u++) dv[u] = ex[u] ? c.trow_base[(int64_t)rv[u] * c.tld + jv[u]] : 0.f;
+                for (int u = 0; u < RB; u++) {
+                    FTI_ASSERT(!ex[u] || (jv[u] < (int)c.tld && (!fa.tab.rowcnt || (int)rv[u] < fa.tab.rowcnt[c.q])));
+                    dv[u] = ex[u] ? c.trow_base[(int64_t)rv[u] * c.tld + jv[u]] : 0.f;
+                }
 #pragma unroll
                 for (int u = 0; u < RB; u++)
                     if (ex[u]) acc = fmaf((float)ex[u], dv[u], acc);

@@ -54,6 +54,8 @@ struct DArgs {
     const uint2* map;          // [nq][nw] {bits, rank} rows of the compact table, or null (row = vocab id)
     const int64_t* row_base;   // [nq] ELEMENT offset of each query's table
     const int32_t* pitch;      // [nq] per-query row pitch (floats)
+    const int32_t* rowcnt;     // [nq] table rows (compact tables), or null: n_rows (FTI_CHECKED bounds only)
+    int64_t n_rows;
     int32_t nw, Sq;
     int unit_w;                // every doc weight is 1
     double* out;
@@ -116,7 +118,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint16_t* myq = queue + warp * DQN * 32 + lane;
     const float* trow = a.table ? a.table + a.row_base[q] : nullptr;
-    const uint32_t ld = a.table ? (uint32_t)a.pitch[q] : 0u;
+    const uint32_t ld = a.table ? (uint32_t)a.pitch[q] : 0u;   // row pitch
+    const int64_t tab_elems = FTI_CHECKED && a.table ? (int64_t)ld * (a.rowcnt ? a.rowcnt[q] : a.n_rows) : 0;
     const uint2* gmapq = a.map ? a.map + (int64_t)q * a.nw : nullptr;
     const uint4* gmh = (const uint4*)(slot + a.L.off_mh);
     const uint16_t* gml = (const uint16_t*)(slot + a.L.off_ml);
@@ -276,8 +279,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
             // ---- root northwest corner, uniform weights ----
             // E / F: cumulative residual boundary of the current doc item i / query item j; o:
             // table-row offset of item i; (rn, on): residual and offset of item i+1; x2: vocab id of
-            // item i+2, x3: raw record of item i+3 (read through pn, which may run past the doc's end
-            // into valid records).  A
+            // item i+2, x3..x5: raw records of items i+3..i+5 (read through pn, which may run past the
+            // doc's end into valid records: the items array carries 8 zero records of padding).  A
             // shared doc item's leftover is U − min(U, W) (its flag comes from the query bitmap); the
             // query side takes its shared items from the queue (qh = query index of the next one).
             // Past a side's last item its boundary grows once beyond the total W·U (no overflow:
@@ -285,15 +288,17 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
             const uint32_t mm = U < W ? U : W, Ud = U - mm, Wq = W - mm;
             auto dres = [&](uint32_t x) { return ((qbits[x >> 5] >> (x & 31)) & 1u) ? Ud : U; };
             int i = 0, j = 0;
-            uint32_t E = 0, F = 0, o = 0, rn = 0, on = 0, x2 = 0, x3 = 0, prev = 0, qh = 0xFFu;
+            uint32_t E = 0, F = 0, o = 0, rn = 0, on = 0, x2 = 0, x3 = 0, x4 = 0, x5 = 0, prev = 0, qh = 0xFFu;
             uint32_t qaddr = (uint32_t)__cvta_generic_to_shared(myq);   // queue head (64 B per entry)
             uint32_t xc = 0, xn = 0;   // EXPORT: vocab ids of items i, i+1
-            const uint2* pn = dit + 4;
+            const uint2* pn = dit + 6;
             if (active) {
                 const uint32_t x0 = dit[0].x & FTI_VOCAB_MASK;
                 const uint32_t x1 = dit[1].x & FTI_VOCAB_MASK;
                 x2 = dit[2].x & FTI_VOCAB_MASK;
                 x3 = dit[3].x;
+                x4 = dit[4].x;
+                x5 = dit[5].x;
                 E = dres(x0);
                 o = EXPORT ? 0u : row_off(x0);
                 rn = dres(x1);
@@ -323,10 +328,13 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     rn = ad ? r2 : rn;
                     on = ad ? o2 : on;
                     if (EXPORT) { xc = ad ? xn : xc; xn = ad ? x2 : xn; }
-                    // raw records two advances ahead: x3 (item i+3) was loaded one advance ago
+                    // raw records loaded three advances before use (x3..x5: items i+3..i+5): the
+                    // record load's latency had been the merge's largest stall
                     if (ad) {
                         x2 = x3 & FTI_VOCAB_MASK;
-                        x3 = pn->x;
+                        x3 = x4;
+                        x4 = x5;
+                        x5 = pn->x;
                     }
                     pn += ad;
                     i += ad;
@@ -347,6 +355,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     acc += (double)part;
 #pragma unroll
                     for (int u = 0; u < DRB; u++) {
+                        FTI_ASSERT(!ef[u] || (int64_t)off[u] < tab_elems);
                         pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
                         pef[u] = ef[u];
                     }
@@ -439,6 +448,7 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     acc += (double)part;
 #pragma unroll
                     for (int u = 0; u < DRB; u++) {
+                        FTI_ASSERT(!ef[u] || (int64_t)off[u] < tab_elems);
                         pdv[u] = ef[u] ? __ldg(trow + off[u]) : 0.f;
                         pef[u] = ef[u];
                     }
@@ -492,6 +502,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     a.table = exp ? nullptr : tab.table;
     a.map = exp ? nullptr : tab.map;
     a.row_base = tab.row_base; a.pitch = tab.pitch;
+    a.rowcnt = tab.rowcnt; a.n_rows = ix->N;
     a.unit_w = ds->unit_w ? 1 : 0;
     a.out = d_out; a.out_ld = out_ld;
     a.fb_list = ds->s_fblist.as<uint32_t>(); a.fb_cnt = ds->s_fbcnt.as<uint32_t>(); a.fb_cap = n_docs;

@@ -42,6 +42,19 @@ ft_status fti_fail(ft_status st, const std::string& msg);
             return fti_fail(FT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
     } while (0)
 
+// FTI_CHECKED builds (python -m paper_1910_04126_b200.build --checked) add device-side bounds
+// assertions on the table gathers and stores, the per-lane queues and the row maps: the stand-in
+// for compute-sanitizer, which this pool does not allow
+#ifndef FTI_CHECKED
+#define FTI_CHECKED 0
+#endif
+#if FTI_CHECKED
+#include <cassert>
+#define FTI_ASSERT(c) assert(c)
+#else
+#define FTI_ASSERT(c) ((void)0)
+#endif
+
 // process-wide options set through ft_set_option (include/flowtree.h); 0 = default
 int64_t fti_opt(int option);
 #define FTI_DBG_DIST 1
@@ -186,6 +199,7 @@ struct FtTable {
     const uint2* map = nullptr;        // [nq][ceil(N/32)] {bits, rank}: row = rank + popc(bits below), or null (row = vocab id)
     const int64_t* row_base = nullptr; // [nq] ELEMENT offset of each query's table
     const int32_t* pitch = nullptr;    // [nq] row pitch (floats) of each query's table
+    const int32_t* rowcnt = nullptr;   // [nq] rows of each compact table (null: every vocab id is a row)
     int64_t rows_cap = 0;
 };
 // lane-per-pair Flowtree with a distance table (ft_flowd.cu), candidate lists or all docs; pairs it

@@ -486,8 +486,8 @@ def test_knn_tiny(ft, prefilter_m):
 
 @pytest.mark.parametrize("n_docs,radix", [(5000, False), (20000, False), (20000, True)])
 def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix):
-    """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id), in
-    order.  n ≤ 8192 sorts the whole row; n = 20000 takes the sample-threshold path (the Quadtree
+    """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id),
+    ordered by (Flowtree value, id) as the oracle ranks it.  n ≤ 8192 sorts the whole row; n = 20000 takes the sample-threshold path (the Quadtree
     values at d = 300 are heavily tied); FT_OPT_SELECT_RADIX forces the MSD radix kernel."""
     if radix:
         opt("FT_OPT_SELECT_RADIX")
@@ -500,7 +500,12 @@ def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix):
         b, bw = wl.query(q)
         qtv = pmap(lambda d: T.qt(*wl.doc(d), b, bw)[1], range(wl.n))
         top = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:m]
-        assert set(ids[q].tolist()) == set(top)
+        assert set(ids[q].tolist()) == set(top)                      # the prefilter: exact
+        # and the returned order is the Flowtree ranking of that set, (value, id) ascending
+        ftv = pmap(lambda d: T.ft(*wl.doc(d), b, bw), top)
+        assert_topk_tieband(ids[q], vals[q], top, ftv, m, what=f"prefilter q{q}")
+        v = vals[q]
+        assert np.all((v[1:] > v[:-1]) | ((v[1:] == v[:-1]) & (ids[q][1:] > ids[q][:-1])))
 
 
 def test_knn_padding_and_errors(ft):
@@ -563,9 +568,16 @@ def test_device_pointers_async_and_sticky_error(ft):
 # ---------------------------------------------------------------------------------------------
 # full size (BASELINE configs, the bench's launch configuration), sampled against the oracle
 # ---------------------------------------------------------------------------------------------
-def test_reviews_full_size_sampled(ft):
+@pytest.mark.parametrize("name,nft,nknn", [("reviews", 8, 6), ("text", 8, 4), ("image", 4, 4), ("stress", 4, 4)])
+def test_full_size_sampled(ft, name, nft, nknn):
+    """Every BASELINE config at its FULL size (reviews n=100k x 1,000 queries; text 10k x 1,000;
+    image 60k x 1,000; stress n=1M x 256-query batch), in the launch shape the bench uses:
+    Quadtree over all docs for the whole batch, bit-exact on sampled pairs; exhaustive Flowtree
+    over all docs for a few queries at the 1e-5 bar on sampled pairs; and the config's k-NN
+    (exhaustive, or the Quadtree prefilter for reviews/stress) against the oracle pipeline over
+    all n docs for several queries, ids exact up to the R15 tie band."""
     import torch
-    wl = get_workload("reviews", n_queries=1000)
+    wl = get_workload(name)
     T = oracle_tree(wl)
     ix, ds = _setup(ft, wl)
     dev = torch.device("cuda:0")
@@ -575,25 +587,29 @@ def test_reviews_full_size_sampled(ft):
     ds.quadtree(wl.q_off, qi, qw, out=out)
     ds.synchronize(torch.cuda.current_stream())
     rng = np.random.default_rng(11)
-    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, wl.nq, 600), rng.integers(0, wl.n, 600))]
-    pairs += [(wl.nq - 1, wl.n - 1), (0, 0)]
-    ref = _oracle_all(T, wl, "qt", pairs)
-    got = out.cpu().numpy()
-    assert np.array_equal(np.array([got[q, d] for q, d in pairs]), np.array([v for _, v in ref]))
-    # Flowtree over all 100k docs for 8 queries, sampled
-    sub = wl.subset_queries(8)
+    qs = np.concatenate([rng.integers(0, wl.nq, 600), [wl.nq - 1, 0]])
+    dd = np.concatenate([rng.integers(0, wl.n, 600), [wl.n - 1, 0]])
+    got = out[torch.from_numpy(qs).to(dev), torch.from_numpy(dd).to(dev)].cpu().numpy()
+    del out
+    ref = _oracle_all(T, wl, "qt", list(zip(qs.tolist(), dd.tolist())))
+    assert np.array_equal(got, np.array([v for _, v in ref])), f"{name} QT"
+    # Flowtree over all docs for nft queries, sampled
+    sub = wl.subset_queries(nft)
     fl = ds.flowtree(sub.q_off, sub.q_ids, sub.q_w)
-    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, 8, 300), rng.integers(0, wl.n, 300))]
-    assert_ft_close([fl[q, d] for q, d in pairs], _oracle_all(T, sub, "ft", pairs), "reviews FT")
-    # k-NN with the BASELINE prefilter, 6 queries, against the oracle pipeline
-    sub = wl.subset_queries(6)
+    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, sub.nq, 300), rng.integers(0, wl.n, 300))]
+    assert_ft_close([fl[q, d] for q, d in pairs], _oracle_all(T, sub, "ft", pairs), f"{name} FT")
+    # k-NN with the config's pipeline for nknn queries against the oracle over all n docs
+    sub = wl.subset_queries(nknn)
     ids, vals = ds.knn(sub.q_off, sub.q_ids, sub.q_w, wl.k, wl.prefilter_m)
     for q in range(sub.nq):
         b, bw = sub.query(q)
-        qtv = pmap(lambda d: T.qt(*wl.doc(d), b, bw)[1], range(wl.n))
-        cand = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:wl.prefilter_m]
+        if wl.prefilter_m:
+            qtv = pmap(lambda d: T.qt(*wl.doc(d), b, bw)[1], range(wl.n))
+            cand = sorted(range(wl.n), key=lambda d: (qtv[d], d))[:wl.prefilter_m]
+        else:
+            cand = list(range(wl.n))
         ftv = pmap(lambda d: T.ft(*wl.doc(d), b, bw), cand)
-        assert_topk_tieband(ids[q], vals[q], cand, ftv, wl.k, what=f"reviews q{q}")
+        assert_topk_tieband(ids[q], vals[q], cand, ftv, wl.k, what=f"{name} q{q}")
 
 
 # ---------------------------------------------------------------------------------------------
