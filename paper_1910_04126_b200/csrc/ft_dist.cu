@@ -56,14 +56,16 @@ constexpr int STAGE_LIMB = TM * KS;      // 8 KB
 constexpr int STAGE_BYTES = NL * STAGE_LIMB;
 constexpr int NSTAGE_MAX = 8;
 constexpr int SBO_A = (KS / 16) * 128;   // A stage: bytes between 8-row core-matrix groups
-constexpr int NBLK = 48;                 // accumulator columns per block (5 tiers × 48 = 240 ≤ 256)
-constexpr int NGRP = 2 * NBLK;           // query columns per work item
-constexpr int SLOT_COLS = 256;           // TMEM columns per accumulator slot
+#ifndef FTD_NBLK
+#define FTD_NBLK 48
+#endif
+constexpr int NBLK = FTD_NBLK;           // accumulator columns per block (5 tiers × NBLK per slot)
+constexpr int NGRP = 96;                 // query columns per work item
+constexpr int NBMAX = NGRP / NBLK;       // blocks per work item
+constexpr int NSLOT = 512 / (5 * NBLK);  // TMEM accumulator slots (2 for 48 columns, 3 for 32)
+constexpr int SLOT_COLS = 5 * NBLK;      // TMEM columns per accumulator slot
 #ifndef FTD_NCOPY
 #define FTD_NCOPY 64
-#endif
-#ifndef FTD_EPI_DB
-#define FTD_EPI_DB 1                     // epilogue: next chunk's tier loads in flight (two register sets)
 #endif
 constexpr int NCOPY = FTD_NCOPY;         // copy threads (warps 0 .. NCOPY/32 − 1)
 constexpr int MMA_WARP = NCOPY / 32;     // warp 2
@@ -241,9 +243,9 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
     uint64_t* bars = (uint64_t*)(eny + NGRP);
     uint64_t* full = bars;                   // [NSTAGE] A stage landed (copy threads, noinc)
     uint64_t* empty = full + NSTAGE_MAX;     // [NSTAGE] A stage consumed (MMA commit)
-    uint64_t* accf = empty + NSTAGE_MAX;     // [2] slot accumulated (MMA commit)
-    uint64_t* acce = accf + 2;               // [2] slot drained (epilogue warps)
-    uint64_t* bfull = acce + 2;              // B landed (complete_tx)
+    uint64_t* accf = empty + NSTAGE_MAX;     // [NSLOT] slot accumulated (MMA commit)
+    uint64_t* acce = accf + NSLOT;           // [NSLOT] slot drained (epilogue warps)
+    uint64_t* bfull = acce + NSLOT;          // B landed (complete_tx)
     uint64_t* bdone = bfull + 1;             // MMAs reading the old B finished (commit)
     uint32_t* tmem_slot = (uint32_t*)(bdone + 1);
     const uint32_t sbo_b = (uint32_t)a.kpad * 8;   // B: (kpad / 16) core matrices × 128 B per 8-row group
@@ -252,7 +254,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
     const int64_t w_begin = T * blockIdx.x / gridDim.x, w_end = T * (blockIdx.x + 1) / gridDim.x;
     if (t == 0) {
         for (int s = 0; s < NSTAGE; s++) { mbar_init(&full[s], NCOPY); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], NEPI); }
+        for (int b = 0; b < NSLOT; b++) { mbar_init(&accf[b], 1); mbar_init(&acce[b], NEPI); }
         mbar_init(bfull, 1);
         mbar_init(bdone, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -330,8 +332,8 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
             const int q = dsc.x, g = dsc.z & 0xFFFF;
             const int cols = dsc.z >> 16;
             const int npad = (cols + 15) & ~15;
-            const int nb = npad > NBLK ? 2 : 1;
-            int nw[2] = {min(npad, NBLK), npad - NBLK};
+            const int nb = (npad + NBLK - 1) / NBLK;
+            auto nw = [&](int b) { return min(NBLK, npad - NBLK * b); };   // block b's width
             if (q != cur_q || g != cur_g) {
                 // reload B once the MMAs reading the previous one have completed
                 if (cur_q >= 0) {
@@ -356,16 +358,17 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 cur_g = g;
             }
             // block b's B region holds its three limbs stacked along N: rows q·nw[b] + j
-            const uint32_t breg[2] = {bbase, bbase + (uint32_t)(3 * nw[0] / 8) * sbo_b};
+            // block b's B region follows the earlier blocks' 3·NBLK rows
+            auto breg = [&](int b) { return bbase + (uint32_t)(3 * NBLK * b / 8) * sbo_b; };
             // one block's MMAs over K stages [c0, c1): A_p · [B_0 | B_1 | B_2] (N = 3·nb) into columns
             // p·nb .. — the product A_p·B_q lands on tier p + q's columns (p + q)·nb, so the nine limb
             // products take three MMAs and every A limb is read once per K step per block
             auto issue = [&](int b, uint32_t dcol, int c, uint32_t st) {
-                const uint32_t n = (uint32_t)nw[b];
+                const uint32_t n = (uint32_t)nw(b);
 #pragma unroll
                 for (int ks = 0; ks < KS / 32; ks++) {
                     const uint32_t kbyte = (uint32_t)(c * KS + ks * 32);
-                    const uint32_t bk = breg[b] + (kbyte >> 4) * 128;
+                    const uint32_t bk = breg(b) + (kbyte >> 4) * 128;
                     auto mma = [&](int pl, int q0, int nq, uint32_t acc) {
                         const uint64_t ad = umma_desc(st + pl * STAGE_LIMB + ks * 256, SBO_A);
                         const uint64_t bd = umma_desc(bk + (uint32_t)(q0 * n / 8) * sbo_b, sbo_b);
@@ -392,8 +395,8 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 }
             };
             auto acquire = [&](int64_t k) {           // the slot of the k-th block, once drained
-                const int sl = (int)(k & 1);
-                if (k >= 2) TW(1, mbar_wait(&acce[sl], (uint32_t)(((k >> 1) - 1) & 1)));
+                const int sl = (int)(k % NSLOT);
+                if (k >= NSLOT) TW(1, mbar_wait(&acce[sl], (uint32_t)((k / NSLOT - 1) & 1)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 return tmem + (uint32_t)sl * SLOT_COLS;
             };
@@ -414,12 +417,12 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                         }
                         __syncwarp();
                     }
-                    if (elect_one()) umma_commit(&accf[(int)((kb + b) & 1)]);
+                    if (elect_one()) umma_commit(&accf[(int)((kb + b) % NSLOT)]);
                     __syncwarp();
                 }
                 fph ^= 1u;
             } else {
-                uint32_t dcol[2];
+                uint32_t dcol[NBMAX];
                 for (int b = 0; b < nb; b++) dcol[b] = acquire(kb + b);
                 for (int c = 0; c < a.nks; c++) {
                     TW(0, mbar_wait(&full[s], fph));
@@ -432,7 +435,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                     if (++s == NSTAGE) { s = 0; fph ^= 1u; }
                 }
                 for (int b = 0; b < nb; b++) {
-                    if (elect_one()) umma_commit(&accf[(int)((kb + b) & 1)]);
+                    if (elect_one()) umma_commit(&accf[(int)((kb + b) % NSLOT)]);
                     __syncwarp();
                 }
             }
@@ -447,32 +450,42 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
         int64_t kb = 0;
         int cur_q = -1, cur_g = -1;
         const uint64_t wpol = FTD_L2POL ? l2_policy_first() : 0ull;
-        // the next item's descriptor, row id, row norm and table placement, loaded one item ahead
-        int4 ndsc = make_int4(0, 0, 0, 0);
-        int32_t nxid = -1, npitch = 8;
+        // per item: descriptor and row id loaded two items ahead, then (depending on them) the row
+        // norm and the table placement one item ahead, so no load's latency is exposed
+        int4 adsc = make_int4(0, 0, 0, 0), ndsc = make_int4(0, 0, 0, 0);
+        int32_t axid = -1, nxid = -1, npitch = 8;
         long long nnx = 0;
         int64_t nrb = 0;
-        auto prefetch = [&](int64_t w) {
+        auto stage_a = [&](int64_t w) {
             if (w < w_end) {
-                ndsc = a.wdesc[w];
-                nxid = a.wrow[w * TM + r];
+                adsc = a.wdesc[w];
+                axid = a.wrow[w * TM + r];
+            }
+        };
+        auto stage_b = [&](int64_t w) {
+            if (w < w_end) {
+                ndsc = adsc;
+                nxid = axid;
                 nnx = nxid >= 0 ? a.xnq[nxid] : 0ll;
                 npitch = a.pitch[ndsc.x];
                 nrb = a.row_base[ndsc.x];
             }
         };
-        prefetch(w_begin);
+        stage_a(w_begin);
+        stage_b(w_begin);
+        stage_a(w_begin + 1);
         for (int64_t w = w_begin; w < w_end; w++) {
             const int4 dsc = ndsc;
             const int32_t xid = nxid;
             const long long nx = nnx;
             const int pitch = npitch;
             const int64_t rbase = nrb;
-            prefetch(w + 1);
+            stage_b(w + 1);
+            stage_a(w + 2);
             const int q = dsc.x, tile = dsc.y, g = dsc.z & 0xFFFF;
             const int cols = dsc.z >> 16;
             const int npad = (cols + 15) & ~15;
-            const int nb = npad > NBLK ? 2 : 1;
+            const int nb = (npad + NBLK - 1) / NBLK;
             if (q != cur_q || g != cur_g) {   // the group's ||ỹ||² (named barrier: epilogue warps only)
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
                 for (int j = et; j < NGRP; j += 32 * NEPI)
@@ -483,31 +496,22 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
             }
             float* trow = a.table + rbase + ((int64_t)tile * TM + r) * pitch + NGRP * g;
             for (int b = 0; b < nb; b++, kb++) {
-                const int sl = (int)(kb & 1);
-                const int nwb = b == 0 ? min(npad, NBLK) : npad - NBLK;   // tier t at columns t·nwb ..
-                // ||ỹ||² of this warp's columns, one per lane (lane l: chunk l >> 3, column l & 7),
-                // read before the wait and broadcast by shuffles: shared-memory loads in the combine
-                // queued behind the tensor core's operand reads (ncu: ≈40% of the combine time)
-                long long nyl = 0;
-                {
-                    const int cidx = 8 * half + 16 * (lane >> 3) + (lane & 7);
-                    if (cidx < nwb) nyl = eny[NBLK * b + cidx];
-                }
-                TW(0, mbar_wait(&accf[sl], (uint32_t)((kb >> 1) & 1)));
+                const int sl = (int)(kb % NSLOT);
+                const int nwb = min(NBLK, npad - NBLK * b);   // tier t at columns t·nwb ..
+                TW(0, mbar_wait(&accf[sl], (uint32_t)((kb / NSLOT) & 1)));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)sl * SLOT_COLS;
                 // chunks of 8 columns, alternating between the quarter's two warps; the next chunk's
                 // five tier loads are in flight while this chunk is combined (two register sets)
                 const bool rowok = xid >= 0;
-                auto combine = [&](const int32_t (&v)[NTIER][8], int c0) {
+                auto combine = [&](const int32_t (&v)[NTIER][8], const long long (&ny)[8], int c0) {
                     const int j0 = NBLK * b + c0;            // column within the group
-                    const int kc = (c0 - 8 * half) >> 4;     // this warp's chunk index (0..2)
                     float o[8];
 #pragma unroll
                     for (int u = 0; u < 8; u++) {
                         // exact: d² = ||v_x||² + ||v_y||² − 2 Σ_t 2^{8t} T_t in int64 (wide
                         // multiply-adds; the 2^33 T4 term only touches the high word), then FP32
-                        long long d2 = nx + __shfl_sync(0xffffffffu, nyl, 8 * kc + u);
+                        long long d2 = nx + ny[u];
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[3][u]), "r"(-(1 << 25)));
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[2][u]), "r"(-(1 << 17)));
                         asm("mad.wide.s32 %0, %1, %2, %0;" : "+l"(d2) : "r"(v[1][u]), "r"(-512));
@@ -526,28 +530,35 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
 #pragma unroll
                     for (int tt = 0; tt < NTIER; tt++) tmem_ld8(tb + (uint32_t)(tt * nwb + c0), v[tt]);
                 };
-#if FTD_EPI_DB
+                // ||ỹ||² of a chunk's 8 columns: read one chunk ahead (with its tier loads), so the
+                // shared-memory latency — long while the tensor core streams operands — is hidden
+                auto loadny = [&](long long (&ny)[8], int c0) {
+#pragma unroll
+                    for (int u = 0; u < 8; u++) ny[u] = eny[NBLK * b + c0 + u];
+                };
                 int32_t va[NTIER][8], vb[NTIER][8];
+                long long ya[8], yb[8];
                 int c0 = 8 * half;
-                if (c0 < nwb) load(va, c0);
+                if (c0 < nwb) {
+                    load(va, c0);
+                    loadny(ya, c0);
+                }
                 while (c0 < nwb) {
                     TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
-                    if (c0 + 16 < nwb) load(vb, c0 + 16);
-                    TW(2, combine(va, c0));
+                    if (c0 + 16 < nwb) {
+                        load(vb, c0 + 16);
+                        loadny(yb, c0 + 16);
+                    }
+                    TW(2, combine(va, ya, c0));
                     if (c0 + 16 >= nwb) break;
                     TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
-                    if (c0 + 32 < nwb) load(va, c0 + 32);
-                    TW(2, combine(vb, c0 + 16));
+                    if (c0 + 32 < nwb) {
+                        load(va, c0 + 32);
+                        loadny(ya, c0 + 32);
+                    }
+                    TW(2, combine(vb, yb, c0 + 16));
                     c0 += 32;
                 }
-#else
-                for (int c0 = 8 * half; c0 < nwb; c0 += 16) {
-                    int32_t va[NTIER][8];
-                    load(va, c0);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    combine(va, c0);
-                }
-#endif
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acce[sl]);
@@ -654,18 +665,19 @@ __global__ void __launch_bounds__(256) k_dist_prep(DistArgs a) {
     int8_t* bg = a.bq + 16 * (size_t)qi.x + (size_t)g * NL * a.kpad * NGRP;
     const size_t rstride = (size_t)a.nks * ROWB;
     const int sbo_b = a.kpad * 8, gran = a.kpad / 16;
-    // block b (columns 48 b ..) stacks its limbs along N: region rows q·nb + j, regions back to back
-    const int nb0 = min(npad, NBLK), nb1 = npad - nb0;
+    // block b (columns NBLK·b ..) stacks its limbs along N: region rows q·nb + j (nb = the block's
+    // width), region b at row 3·NBLK·b
     const int total = NL * npad * gran;                    // thread per (region row, 16-byte K granule)
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int kg = e % gran, rr = e / gran;            // rr: row over both regions
-        const int b = rr < 3 * nb0 ? 0 : 1;
-        const int rb = b ? rr - 3 * nb0 : rr, nbw = b ? nb1 : nb0;
+        const int kg = e % gran, rr = e / gran;            // rr: row over the packed regions
+        int b = 0, rb = rr;
+        while (rb >= 3 * min(NBLK, npad - NBLK * b)) { rb -= 3 * min(NBLK, npad - NBLK * b); b++; }
+        const int nbw = min(NBLK, npad - NBLK * b);
         const int p = rb / nbw, j = NBLK * b + rb % nbw;  // limb, query column within the group
         const int64_t src = j < cols ? (int64_t)yid[j] : a.N;     // the zero row pads the group
         const int c = kg / (KS / 16), kb = (kg % (KS / 16)) * 16;
         const uint4 v = *(const uint4*)(a.Xq + src * rstride + (size_t)c * ROWB + p * KS + kb);
-        *(uint4*)(bg + (size_t)(b ? 3 * nb0 : 0) * a.kpad + cm_off(rb, 16 * kg, sbo_b)) = v;
+        *(uint4*)(bg + (size_t)(3 * NBLK * b) * a.kpad + cm_off(rb, 16 * kg, sbo_b)) = v;
     }
 }
 
