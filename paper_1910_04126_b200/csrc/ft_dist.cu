@@ -69,8 +69,21 @@ constexpr int SLOT_COLS = 5 * NBLK;      // TMEM columns per accumulator slot
 #endif
 constexpr int NCOPY = FTD_NCOPY;         // copy threads (warps 0 .. NCOPY/32 − 1)
 constexpr int MMA_WARP = NCOPY / 32;     // warp 2
-constexpr int NEPI = 8;                  // epilogue warps 3-10 (11 warps: ≤ 3 per SM sub-partition,
-                                         // so up to 168 registers per thread)
+#ifndef FTD_NEPI
+#define FTD_NEPI 8
+#endif
+#ifndef FTD_ABL
+#define FTD_ABL 0          // ablation (timing experiments only; wrong tables): 1 no copies, 2 no MMAs,
+                           // 4 no epilogue work, 8 no table stores
+#endif
+#ifndef FTD_REV
+#define FTD_REV 0          // block-outer order: the item's narrowest (last) block first
+#endif
+#ifndef FTD_EDB
+#define FTD_EDB 1          // epilogue: the next chunk's TMEM loads in flight while one is combined
+#endif
+constexpr int NEPI = FTD_NEPI;           // epilogue warps (a multiple of 4: NEPI / 4 per TMEM lane quarter)
+constexpr int NPART = NEPI / 4;          // epilogue warps per quarter, on interleaved 8-column chunks
 constexpr int NTHREADS = NCOPY + 32 + 32 * NEPI;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int QMAX_ABS = (1 << 23) - (1 << 16);   // |v| bound: the top balanced limb stays in [−128, 127]
@@ -126,8 +139,28 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+#ifndef FTD_CPCA
+#define FTD_CPCA 0         // 1: cp.async.ca (through L1) instead of .cg
+#endif
+#ifndef FTD_KOUTER
+#define FTD_KOUTER 0       // 1: K-outer MMA order with the deepest ring that fits (test option)
+#endif
+#ifndef FTD_LDGCP
+#define FTD_LDGCP 0        // 1: copy warps load 32-byte sectors into registers and st.shared them
+#endif
+#ifndef FTD_ST256
+#define FTD_ST256 1        // one 256-bit store per row chunk of 8 distances (one full sector; 0: two 16-byte stores)
+#endif
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    if (FTD_CPCA)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void st_f8(float* p, const float (&o)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                 "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
+                 : "memory");
 }
 __device__ __forceinline__ void cp_async16_pol(uint32_t dst, const void* src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
@@ -223,7 +256,7 @@ __device__ unsigned long long g_dbg[16];
 
 template <bool DBG>
 // NTHREADS threads, one CTA per SM; ≤ 3 warps per SM sub-partition leave 168 registers a thread
-#if (FTD_NCOPY / 32 + 1 + 8) <= 12
+#if (FTD_NCOPY / 32 + 1 + FTD_NEPI) <= 12
 #define FTD_KATTR __maxnreg__(168)
 #else
 #define FTD_KATTR __launch_bounds__(NTHREADS, 1)
@@ -269,7 +302,98 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
 
-    if (t < NCOPY) {
+    if (FTD_LDGCP && t < NCOPY) {
+        // ------------------------------------------------------------------ copy threads (LDG path)
+        // 32-byte register loads (each lane one full sector: 16-byte cp.async requests fetch every
+        // sector twice) stored to the ring with st.shared, then a proxy fence and an arrive.  Warp
+        // cw fills rows 64 cw .. +63; per stage it issues 12 load slots over 4 pairs of 8-row
+        // groups (3 per pair: units 0-3 of each group, then units 4-5 of both), in two halves of 6
+        // slots that are double buffered in registers.  Unit k of a row = limb k / 2, 32-byte half
+        // k % 2 of the stage's 64 coordinates.
+        static_assert(NCOPY == 64, "LDG copy path: two copy warps");
+        const int cw = warp;
+        const uint32_t abase = smem_u32(aring);
+        const size_t rstride = (size_t)a.nks * ROWB;
+        // slot sl (pair pp = sl / 3, kind = sl % 3) of this lane: its 8-row group selector, unit k
+        auto slot_g = [&](int sl) { return sl % 3 == 2 ? (lane >> 4) : sl % 3; };
+        auto slot_k = [&](int sl) { return sl % 3 == 2 ? 4 + ((lane >> 3) & 1) : (lane >> 3); };
+        auto slot_dof = [&](int sl) {
+            const int k = slot_k(sl);
+            const int r = 8 * (2 * (4 * cw + sl / 3) + slot_g(sl)) + (lane & 7);
+            return (uint32_t)((k >> 1) * STAGE_LIMB) + cm_off(r, 32 * (k & 1), SBO_A);
+        };
+        auto rowid = [&](int64_t w, int j) {   // row id j of the lane in item w (−1 → zero row)
+            const int pp = j >> 1, gsel = j & 1;
+            const int32_t x = a.wrow[w * TM + 8 * (2 * (4 * cw + pp) + gsel) + (lane & 7)];
+            return x >= 0 ? x : (int32_t)a.N;
+        };
+        int32_t px[8];
+        if (w_begin < w_end)
+#pragma unroll
+            for (int j = 0; j < 8; j++) px[j] = rowid(w_begin, j);
+        uint32_t ra[6][8], rb[6][8];
+        auto ld8 = [&](uint32_t (&r)[8], const int8_t* g) {
+            if (!(FTD_ABL & 1))
+                asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                               "=r"(r[7])
+                             : "l"(g));
+        };
+        auto st8 = [&](uint32_t dst, const uint32_t (&r)[8]) {
+            if (!(FTD_ABL & 1)) {
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                             "r"(r[3])
+                             : "memory");
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 128u), "r"(r[4]), "r"(r[5]),
+                             "r"(r[6]), "r"(r[7])
+                             : "memory");
+            }
+        };
+        // half hf of stage c of the item whose row ids are px
+        auto load_half = [&](uint32_t (&r)[6][8], const int32_t (&rows)[8], int c, int hf) {
+#pragma unroll
+            for (int u = 0; u < 6; u++) {
+                const int sl = 6 * hf + u;
+                const int32_t x = rows[2 * (sl / 3) + (sl % 3 == 2 ? 0 : sl % 3)];
+                const int32_t x1 = rows[2 * (sl / 3) + 1];
+                const int32_t xr = (sl % 3 == 2 && (lane >> 4)) ? x1 : x;
+                ld8(r[u], a.Xq + (size_t)xr * rstride + (size_t)c * ROWB + 32 * slot_k(sl));
+            }
+        };
+        auto store_half = [&](const uint32_t (&r)[6][8], uint32_t st, int hf) {
+#pragma unroll
+            for (int u = 0; u < 6; u++) st8(st + slot_dof(6 * hf + u), r[u]);
+        };
+        int s = 0;
+        uint32_t eph = 0;
+        bool first = true;
+        if (w_begin < w_end) load_half(ra, px, 0, 0);
+        for (int64_t w = w_begin; w < w_end; w++) {
+            int32_t pn[8];
+            const bool more = w + 1 < w_end;
+            if (more)
+#pragma unroll
+                for (int j = 0; j < 8; j++) pn[j] = rowid(w + 1, j);
+            for (int c = 0; c < a.nks; c++) {
+                load_half(rb, px, c, 1);
+                if (!first) TW(0, mbar_wait(&empty[s], eph));
+                const uint32_t st = abase + (uint32_t)s * STAGE_BYTES;
+                store_half(ra, st, 0);
+                if (c + 1 < a.nks) load_half(ra, px, c + 1, 0);
+                else if (more) load_half(ra, pn, 0, 0);
+                store_half(rb, st, 1);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&full[s]);
+                if (++s == NSTAGE) {
+                    s = 0;
+                    if (first) first = false; else eph ^= 1u;
+                }
+            }
+            if (more)
+#pragma unroll
+                for (int j = 0; j < 8; j++) px[j] = pn[j];
+        }
+    } else if (t < NCOPY) {
         // ------------------------------------------------------------------ copy threads
         // lane → (row & 7, 16-byte granule): one cp.async instruction per limb moves 8 rows × 64
         // contiguous bytes (full sectors); warp cw fills rows 64 cw .. +63 of every stage
@@ -303,7 +427,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 for (int p = 0; p < NL; p++)
 #pragma unroll
                     for (int rg = 0; rg < RG; rg++)
-                        if (grp_ok(rg)) {
+                        if (grp_ok(rg) && !(FTD_ABL & 1)) {
                             if (FTD_L2POL) cp_async16_pol(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS, pol);
                             else cp_async16(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS);
                         }
@@ -373,7 +497,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                         const uint64_t ad = umma_desc(st + pl * STAGE_LIMB + ks * 256, SBO_A);
                         const uint64_t bd = umma_desc(bk + (uint32_t)(q0 * n / 8) * sbo_b, sbo_b);
                         const uint32_t idesc = idesc0 | ((uint32_t)(nq * n >> 3) << 17);
-                        asm volatile(
+                        if (!(FTD_ABL & 2)) asm volatile(
                             "{\n\t.reg .pred pr;\n\tsetp.ne.b32 pr, %4, 0;\n\t"
                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pr;\n\t}" ::"r"(
                                 dcol + (uint32_t)(pl + q0) * n),
@@ -404,20 +528,21 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 // the ring holds the tile's whole K range (stage = K step): block-outer order, so
                 // block 0's accumulator is committed (and drained by the epilogue) while block 1
                 // computes; a stage is released after the last block has read it
-                for (int b = 0; b < nb; b++) {
-                    const uint32_t dcol = acquire(kb + b);
+                for (int i = 0; i < nb; i++) {
+                    const int b = FTD_REV ? nb - 1 - i : i;    // block i of the item's sequence
+                    const uint32_t dcol = acquire(kb + i);
                     for (int c = 0; c < a.nks; c++) {
-                        if (b == 0) {
+                        if (i == 0) {
                             TW(0, mbar_wait(&full[c], fph));
                             asm volatile("tcgen05.fence::after_thread_sync;");
                         }
                         if (elect_one()) {
                             issue(b, dcol, c, abase + (uint32_t)c * STAGE_BYTES);
-                            if (b == nb - 1) umma_commit(&empty[c]);
+                            if (i == nb - 1) umma_commit(&empty[c]);
                         }
                         __syncwarp();
                     }
-                    if (elect_one()) umma_commit(&accf[(int)((kb + b) % NSLOT)]);
+                    if (elect_one()) umma_commit(&accf[(int)((kb + i) % NSLOT)]);
                     __syncwarp();
                 }
                 fph ^= 1u;
@@ -444,7 +569,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
     } else {
         // ------------------------------------------------------------------ epilogue
         const int quarter = warp & 3;                 // TMEM lanes 32·quarter .. +31 (hardware rule)
-        const int half = (warp - MMA_WARP - 1) >> 2;  // which alternate 8-column chunks this warp takes
+        const int part = (warp - MMA_WARP - 1) >> 2;  // which interleaved 8-column chunks this warp takes
         const int et = t - (NCOPY + 32);              // 0 .. 32·NEPI − 1
         const int r = quarter * 32 + lane;            // tile row = TMEM lane
         int64_t kb = 0;
@@ -495,7 +620,8 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 cur_g = g;
             }
             float* trow = a.table + rbase + ((int64_t)tile * TM + r) * pitch + NGRP * g;
-            for (int b = 0; b < nb; b++, kb++) {
+            for (int i = 0; i < nb; i++, kb++) {
+                const int b = (FTD_REV && a.blk_outer) ? nb - 1 - i : i;
                 const int sl = (int)(kb % NSLOT);
                 const int nwb = min(NBLK, npad - NBLK * b);   // tier t at columns t·nwb ..
                 TW(0, mbar_wait(&accf[sl], (uint32_t)((kb / NSLOT) & 1)));
@@ -521,10 +647,14 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                         asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(u57_to_f32((unsigned long long)d2)));
                         o[u] = sq * a.scale;
                     }
-                    if (!rowok || NGRP * g + j0 >= pitch) return;
+                    if (!rowok || NGRP * g + j0 >= pitch || (FTD_ABL & 8)) return;
                     FTI_ASSERT(NGRP * g + j0 + 8 <= pitch && (!a.rowcnt || (int64_t)tile * TM + r < a.rowcnt[q]));
-                    st_f4(trow + j0, make_float4(o[0], o[1], o[2], o[3]), wpol);
-                    st_f4(trow + j0 + 4, make_float4(o[4], o[5], o[6], o[7]), wpol);
+                    if (FTD_ST256) {
+                        st_f8(trow + j0, o);
+                    } else {
+                        st_f4(trow + j0, make_float4(o[0], o[1], o[2], o[3]), wpol);
+                        st_f4(trow + j0 + 4, make_float4(o[4], o[5], o[6], o[7]), wpol);
+                    }
                 };
                 auto load = [&](int32_t (&v)[NTIER][8], int c0) {
 #pragma unroll
@@ -536,28 +666,43 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
 #pragma unroll
                     for (int u = 0; u < 8; u++) ny[u] = eny[NBLK * b + c0 + u];
                 };
-                int32_t va[NTIER][8], vb[NTIER][8];
-                long long ya[8], yb[8];
-                int c0 = 8 * half;
-                if (c0 < nwb) {
-                    load(va, c0);
-                    loadny(ya, c0);
-                }
-                while (c0 < nwb) {
-                    TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
-                    if (c0 + 16 < nwb) {
-                        load(vb, c0 + 16);
-                        loadny(yb, c0 + 16);
+                constexpr int STEP = 8 * NPART;
+                int32_t va[NTIER][8];
+                long long ya[8];
+                int c0 = 8 * part;
+                if (FTD_ABL & 4) c0 = nwb;
+                if (FTD_EDB) {
+                    int32_t vb[NTIER][8];
+                    long long yb[8];
+                    if (c0 < nwb) {
+                        load(va, c0);
+                        loadny(ya, c0);
                     }
-                    TW(2, combine(va, ya, c0));
-                    if (c0 + 16 >= nwb) break;
-                    TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
-                    if (c0 + 32 < nwb) {
-                        load(va, c0 + 32);
-                        loadny(ya, c0 + 32);
+                    while (c0 < nwb) {
+                        TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
+                        if (c0 + STEP < nwb) {
+                            load(vb, c0 + STEP);
+                            loadny(yb, c0 + STEP);
+                        }
+                        TW(2, combine(va, ya, c0));
+                        if (c0 + STEP >= nwb) break;
+                        TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
+                        if (c0 + 2 * STEP < nwb) {
+                            load(va, c0 + 2 * STEP);
+                            loadny(ya, c0 + 2 * STEP);
+                        }
+                        TW(2, combine(vb, yb, c0 + STEP));
+                        c0 += 2 * STEP;
                     }
-                    TW(2, combine(vb, yb, c0 + 16));
-                    c0 += 32;
+                } else {
+                    // more epilogue warps instead: the other warps of the SM sub-partition hide the
+                    // TMEM load latency
+                    for (; c0 < nwb; c0 += STEP) {
+                        load(va, c0);
+                        loadny(ya, c0);
+                        TW(1, asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"));
+                        TW(2, combine(va, ya, c0));
+                    }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
@@ -882,9 +1027,9 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     // 2..4 stages (K-outer order)
     int nstage = a.nks;
     a.blk_outer = 1;
-    if (nstage > NSTAGE_MAX || dist_smem(nstage, a.kpad) > 227 * 1024) {
+    if (FTD_KOUTER || nstage > NSTAGE_MAX || dist_smem(nstage, a.kpad) > 227 * 1024) {
         a.blk_outer = 0;
-        nstage = 4;
+        nstage = FTD_KOUTER ? NSTAGE_MAX : 4;
         while (nstage > 2 && dist_smem(nstage, a.kpad) > 227 * 1024) nstage--;
     }
     a.nstage = nstage;

@@ -15,7 +15,7 @@ $Q > gpurun_out/kp_qt.log 2>&1 && \
 echo "qt rc=$?"
 K="python tools/kprof.py knn --queries 1000 --reps 1"
 $K > gpurun_out/kp_knn.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_dist_tc|k_ftd|k_flowtree|k_select_fast|k_vocab|k_qt_dense|k_tiles|k_dist_prep|k_tile_plan" -c 9 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_dist_i8|k_ftd|k_flowtree|k_select_fast|k_vocab|k_qt_dense|k_tiles|k_dist_prep|k_tile_plan" -c 9 \
   -o gpurun_out/prof_knn $K > gpurun_out/ncu_knn.log 2>&1
 echo "knn rc=$?"
 X="python tools/kprof.py ft --queries 64 --reps 1"
