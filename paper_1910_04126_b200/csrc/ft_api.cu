@@ -479,17 +479,13 @@ extern "C" ft_status ft_knn(const ft_dataset* cds, const int64_t* q_off, int32_t
                                    st));
     } else {
         const int64_t m = prefilter_m;
-        FTI_RES(ds->s_vals, sizeof(double) * nq * n);
         FTI_RES(ds->s_cand, sizeof(int64_t) * nq * m);
         FTI_RES(ds->s_vals2, sizeof(double) * nq * m);
         {
+            // Quadtree + top-m (fused: the stage time is reported under "quadtree")
             StageTimer tm(ds, FTI_ST_QT, st);
-            FTI_CUDA(fti_launch_qt(ds, S.L, S.qblock, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st));
-        }
-        {
-            StageTimer tm(ds, FTI_ST_SELM, st);
-            FTI_CUDA(fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m,
-                                       ds->s_cand.as<int64_t>(), ds->s_vals2.as<double>(), m, sel_scratch, st));
+            FTI_CUDA(fti_launch_prefilter(ds, S.L, S.qblock, nq, m, ds->s_cand.as<int64_t>(), ds->s_vals2.as<double>(),
+                                          sel_scratch, st));
         }
         rc = flowtree_stage(ds, S, nq, ds->s_cand.as<int64_t>(), m, m, ds->s_vals2.as<double>(), m, st);
         if (rc) return rc;

@@ -60,7 +60,10 @@ constexpr int SBO_A = (KS / 16) * 128;   // A stage: bytes between 8-row core-ma
 #define FTD_NBLK 48
 #endif
 constexpr int NBLK = FTD_NBLK;           // accumulator columns per block (5 tiers × NBLK per slot)
-constexpr int NGRP = 96;                 // query columns per work item
+#ifndef FTD_NGRP
+#define FTD_NGRP 96
+#endif
+constexpr int NGRP = FTD_NGRP;           // query columns per work item
 constexpr int NBMAX = NGRP / NBLK;       // blocks per work item
 constexpr int NSLOT = 512 / (5 * NBLK);  // TMEM accumulator slots (2 for 48 columns, 3 for 32)
 constexpr int SLOT_COLS = 5 * NBLK;      // TMEM columns per accumulator slot
@@ -448,6 +451,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
         int s = 0;
         uint32_t fph = 0, bph = 0, dph = 0;
         int64_t kb = 0;            // accumulator blocks issued so far (slot = kb & 1)
+        int64_t it0 = 0;           // ring stages consumed so far (block-outer order)
         int cur_q = -1, cur_g = -1;
         int4 ndsc = w_begin < w_end ? a.wdesc[w_begin] : make_int4(0, 0, 0, 0);
         for (int64_t w = w_begin; w < w_end; w++) {
@@ -528,24 +532,29 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 // the ring holds the tile's whole K range (stage = K step): block-outer order, so
                 // block 0's accumulator is committed (and drained by the epilogue) while block 1
                 // computes; a stage is released after the last block has read it
+                // (the ring may be deeper than a tile: stage c of the item is ring slot
+                // (it0 + c) mod NSTAGE, so the next item's first stages load while this one computes)
                 for (int i = 0; i < nb; i++) {
                     const int b = FTD_REV ? nb - 1 - i : i;    // block i of the item's sequence
                     const uint32_t dcol = acquire(kb + i);
+                    int sc = (int)(it0 % NSTAGE);
+                    uint32_t ph = (uint32_t)((it0 / NSTAGE) & 1);
                     for (int c = 0; c < a.nks; c++) {
                         if (i == 0) {
-                            TW(0, mbar_wait(&full[c], fph));
+                            TW(0, mbar_wait(&full[sc], ph));
                             asm volatile("tcgen05.fence::after_thread_sync;");
                         }
                         if (elect_one()) {
-                            issue(b, dcol, c, abase + (uint32_t)c * STAGE_BYTES);
-                            if (i == nb - 1) umma_commit(&empty[c]);
+                            issue(b, dcol, c, abase + (uint32_t)sc * STAGE_BYTES);
+                            if (i == nb - 1) umma_commit(&empty[sc]);
                         }
                         __syncwarp();
+                        if (++sc == NSTAGE) { sc = 0; ph ^= 1u; }
                     }
                     if (elect_one()) umma_commit(&accf[(int)((kb + i) % NSLOT)]);
                     __syncwarp();
                 }
-                fph ^= 1u;
+                it0 += a.nks;
             } else {
                 uint32_t dcol[NBMAX];
                 for (int b = 0; b < nb; b++) dcol[b] = acquire(kb + b);
@@ -1025,13 +1034,10 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.wrow = ds->s_wrow.as<int32_t>();
     // the whole K range of a tile resident (block-outer MMA order) when it fits, else a ring of
     // 2..4 stages (K-outer order)
-    int nstage = a.nks;
-    a.blk_outer = 1;
-    if (FTD_KOUTER || nstage > NSTAGE_MAX || dist_smem(nstage, a.kpad) > 227 * 1024) {
-        a.blk_outer = 0;
-        nstage = FTD_KOUTER ? NSTAGE_MAX : 4;
-        while (nstage > 2 && dist_smem(nstage, a.kpad) > 227 * 1024) nstage--;
-    }
+    int nstage = NSTAGE_MAX;
+    while (nstage > 2 && dist_smem(nstage, a.kpad) > 227 * 1024) nstage--;
+    a.blk_outer = (!FTD_KOUTER && nstage >= a.nks) ? 1 : 0;
+    if (!a.blk_outer && !FTD_KOUTER) nstage = std::min(nstage, 4);
     a.nstage = nstage;
     const size_t smem = dist_smem(nstage, a.kpad);
     const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_DIST) != 0;

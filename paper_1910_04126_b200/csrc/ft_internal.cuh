@@ -18,6 +18,7 @@
 #define FTI_MAX_SUPPORT 2048        // max support size of one distribution (doc or query)
 #define FTI_MAX_NODE_ENTRIES 8192   // max support * depth entries per distribution
 #define FTI_MAX_SELECT 8192         // max k / prefilter_m handled by the selection kernel
+#define FTI_PREFILTER_CAP 32768     // candidate-list capacity per query of the fused prefilter
 #define FTI_MAX_WEIGHT_TOTAL 65535u // W, U <= 65535 keeps W*U < 2^32
 #define FTI_VOCAB_MASK 0x3FFFFFFFu  // vocab ids < 2^30; bits 30/31 of an item word are flags
 #define FTI_FLAG_MULTI_LEAF 0x80000000u  // the item's leaf holds >= 2 ground points
@@ -180,6 +181,9 @@ struct ft_dataset {
     // scratch (grow-only; reused across calls)
     DevBuf s_pitch, s_qoff, s_qids, s_qw, s_qblock, s_docs, s_vals, s_vals2, s_cand, s_outid, s_outval;
     DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_topk;
+    // fused prefilter (fti_launch_prefilter): sample doc ids, sample values, thresholds, lists
+    DevBuf s_pf_samp, s_pf_sval, s_pf_tval, s_pf_cnt, s_pf_cval, s_pf_cid, s_pf_bad, s_pf_flag;
+    int64_t pf_ns = -1;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -191,6 +195,9 @@ QueryLayout fti_query_layout(const ft_index* ix, int32_t smax);
 cudaError_t fti_launch_query_prep(const ft_index* ix, const QueryLayout& L, const int64_t* d_qoff, int32_t nq,
                                   const int32_t* d_qids, const uint32_t* d_qw, uint8_t* d_qblock,
                                   uint32_t* d_err, cudaStream_t st);
+// a3 + a4: per query the m smallest (Quadtree value, doc id) over all docs (fused when n ≥ 32·m)
+cudaError_t fti_launch_prefilter(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t m,
+                                 int64_t* d_cand, double* d_cval, int* d_sel_scratch, cudaStream_t st);
 cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
                           const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
                           cudaStream_t st);
@@ -230,4 +237,9 @@ cudaError_t fti_launch_vocab_map(const ft_dataset* ds, int32_t nq, const int64_t
                                  cudaStream_t st);
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
-                              int* d_scratch /* rows + 1 ints */, cudaStream_t st, int64_t id_base = 0);
+                              int* d_scratch /* rows + 1 ints */, cudaStream_t st, int64_t id_base = 0,
+                              const uint32_t* d_row_len = nullptr, const int* d_rows_list = nullptr,
+                              const int* d_nrows_list = nullptr, int* d_bad = nullptr, bool nosort = false);
+// per row, a value ≥ the r-th smallest (0-based) of L values within FP32 rounding (prefilter threshold)
+cudaError_t fti_launch_row_threshold(const double* d_vals, int64_t ld, int64_t L, int32_t rows, int64_t r,
+                                     double* d_thr, cudaStream_t st);

@@ -282,11 +282,21 @@ struct QtArgs {
     double pow2;                // 2^{ℓ_root − D*} when it is a normal double (0: use scalbn)
     int wide;                   // D* > 31: the U·A and W·B products can overflow 64 bits
     uint32_t* err;
+    // threshold mode (the fused prefilter): instead of writing out, append (value, doc) to query q's
+    // candidate list when value ≤ thr[q·thr_ld]; ccnt counts every passing doc (also past ccap)
+    const double* thr;
+    int64_t thr_ld;
+    uint32_t* ccnt;
+    double* cval;
+    int64_t* cid;
+    int64_t ccap;
+    // fallback mode: only the chunks holding a flagged query run, and only flagged rows are written
+    const uint32_t* qflag;
 };
 
 // lane q: QT(q, doc) = (U A + W B_q − 2 acc) · 2^{ℓ_root − D*} / (W U), exact u64 numerator, two
 // correctly rounded FP64 operations (NaN for an invalid query or an overflowing numerator)
-__device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int64_t dp,
+__device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int64_t dp, int64_t doc,
                                          unsigned long long acc, uint32_t W32, unsigned long long A) {
     const int lane = threadIdx.x & 31;
     if (lane >= nqc) return;
@@ -311,6 +321,17 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
         const double scaled = a.pow2 != 0.0 ? (double)num * a.pow2 : scalbn((double)num, a.l_root - a.d_star);
         val = __ddiv_rn(scaled, (double)(Uq * W));
     }
+    if (a.thr) {
+        if (!bad && val <= a.thr[(int64_t)q * a.thr_ld]) {
+            const uint32_t pos = atomicAdd(&a.ccnt[q], 1u);
+            if ((int64_t)pos < a.ccap) {
+                a.cval[(int64_t)q * a.ccap + pos] = val;
+                a.cid[(int64_t)q * a.ccap + pos] = doc;
+            }
+        }
+        return;
+    }
+    if (a.qflag && !a.qflag[q]) return;
     a.out[(int64_t)q * a.out_ld + dp] = val;
 }
 
@@ -331,7 +352,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
     for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
         const int64_t doc = a.docs ? a.docs[dp] : dp;
         if (doc < 0 || doc >= a.n) {
-            if (lane < nqc)
+            if (lane < nqc && !a.thr)
                 a.out[(int64_t)(blockIdx.y * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
             if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
             continue;
@@ -383,7 +404,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             }
             __syncwarp();
         }
-        qt_store(a, sh, nqc, dp, acc, W32, A);
+        qt_store(a, sh, nqc, dp, doc, acc, W32, A);
     }
 }
 
@@ -404,7 +425,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
     for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
         const int64_t doc = a.docs ? a.docs[dp] : dp;
         if (doc < 0 || doc >= a.n) {
-            if (lane < nqc) a.out[(int64_t)q * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+            if (lane < nqc && !a.thr) a.out[(int64_t)q * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
             if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
             continue;
         }
@@ -448,7 +469,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 visit(e2, m2);
             }
         }
-        qt_store(a, sh, nqc, dp, acc, W32, A);
+        qt_store(a, sh, nqc, dp, doc, acc, W32, A);
     }
 }
 
@@ -460,6 +481,14 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
     uint2* ent_s = (uint2*)(keys + g.cap);                // ucap_s {query mask, posting offset}
     uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
     uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
+    if (a.qflag) {   // fallback mode: chunks without a flagged query have nothing to do
+        int f = 0;
+        if (threadIdx.x < QT_QC) {
+            const int q = blockIdx.y * QT_QC + threadIdx.x;
+            f = q < a.nq && a.qflag[q] != 0u;
+        }
+        if (!__syncthreads_or(f)) return;
+    }
     const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
     __shared__ DenseHdr dh;
     const uint8_t* dsrc = a.dchunks ? a.dchunks + (size_t)blockIdx.y * a.dg.stride : nullptr;
@@ -508,22 +537,32 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
 
 }  // namespace
 
-cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
-                          const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
-                          cudaStream_t st) {
-    (void)docs_ld;   // the Quadtree stage always scores one doc list shared by the batch
-    if (nq <= 0 || n_docs <= 0) return cudaSuccess;
-    const ChunkGeom g = chunk_geom(ds, L);
-    const int nchunks = (nq + QT_QC - 1) / QT_QC;
-    cudaError_t e = ds->s_chunk.reserve(g.stride * (size_t)nchunks);
+namespace {
+
+// chunk structures of a query batch (shared by every scan of the batch) and the scan's geometry
+struct QtPlan {
+    ChunkGeom g;
+    DenseGeom dg;
+    int nchunks;
+    size_t smem;
+    int ctas_per_sm;
+};
+
+cudaError_t qt_prepare(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, cudaStream_t st,
+                       QtPlan& P) {
+    P.g = chunk_geom(ds, L);
+    P.nchunks = (nq + QT_QC - 1) / QT_QC;
+    cudaError_t e = ds->s_chunk.reserve(P.g.stride * (size_t)P.nchunks);
     if (e != cudaSuccess) return e;
-    size_t smem_c = 4ull * g.cap + 8ull * g.umax + 2ull * g.cap;
+    size_t smem_c = 4ull * P.g.cap + 8ull * P.g.umax + 2ull * P.g.cap;
     if (smem_c > 220 * 1024) return cudaErrorInvalidConfiguration;   // query batch too large for one chunk
     e = cudaFuncSetAttribute(k_qt_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
     if (e != cudaSuccess) return e;
-    k_qt_chunk<<<nchunks, 1024, smem_c, st>>>(d_qblock, L, nq, g, ds->s_chunk.as<uint8_t>(), ds->err_dev);
+    k_qt_chunk<<<P.nchunks, 1024, smem_c, st>>>(d_qblock, L, nq, P.g, ds->s_chunk.as<uint8_t>(), ds->err_dev);
+    fti_count_launches(1);
     // dense structure: node-id bitmap + ranks in shared memory (M ≤ ~393k nodes), union ≤ cap
-    DenseGeom dg{};
+    DenseGeom& dg = P.dg;
+    dg = DenseGeom{};
     dg.mw = (int)((ds->ix->M + 31) / 32);
     const size_t dense_budget = 200 * 1024;
     dg.cap = 0;
@@ -531,41 +570,150 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
         dg.cap = (int)std::min<size_t>(2048, (dense_budget - (size_t)dg.mw * 8) / (QT_QC * 2)) & ~31;
     dg.stride = (sizeof(DenseHdr) + (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 15) / 16 * 16;
     if (dg.cap > 0) {
-        e = ds->s_chunkd.reserve(dg.stride * (size_t)nchunks);
+        e = ds->s_chunkd.reserve(dg.stride * (size_t)P.nchunks);
         if (e != cudaSuccess) return e;
         const size_t smem_d = (size_t)dg.mw * 8;
         e = cudaFuncSetAttribute(k_qt_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
         if (e != cudaSuccess) return e;
-        k_qt_dense<<<nchunks, 1024, smem_d, st>>>(d_qblock, L, nq, dg, ds->s_chunkd.as<uint8_t>());
+        k_qt_dense<<<P.nchunks, 1024, smem_d, st>>>(d_qblock, L, nq, dg, ds->s_chunkd.as<uint8_t>());
         fti_count_launches(1);
     }
-    QtArgs a{};
+    P.smem = std::max<size_t>(4ull * P.g.cap + 8ull * P.g.ucap_s + 4ull * P.g.pcap_s + 2ull * P.g.cap,
+                              dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 16 + (size_t)QT_WARPS * 32 * 16
+                                         : 0);
+    e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem);
+    if (e != cudaSuccess) return e;
+    P.ctas_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&P.ctas_per_sm, k_qt, QT_WARPS * 32, P.smem);
+    P.ctas_per_sm = std::max(1, P.ctas_per_sm);
+    return cudaSuccess;
+}
+
+// one scan of n_docs docs (d_docs, or all) with the prepared chunks; `mode` carries the threshold /
+// fallback fields (zero: plain values into d_out)
+cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* d_docs, int64_t n_docs, double* d_out,
+                    int64_t out_ld, const QtArgs& mode, int waves, cudaStream_t st) {
+    QtArgs a = mode;
     a.qt_off = ds->qt_off; a.qt = ds->qt; a.W = ds->W; a.A = ds->A;
-    a.chunks = ds->s_chunk.as<uint8_t>(); a.g = g;
-    a.dchunks = dg.cap > 0 ? ds->s_chunkd.as<uint8_t>() : nullptr; a.dg = dg;
+    a.chunks = ds->s_chunk.as<uint8_t>(); a.g = P.g;
+    a.dchunks = P.dg.cap > 0 ? ds->s_chunkd.as<uint8_t>() : nullptr; a.dg = P.dg;
     a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
     a.pow2 = std::abs(a.l_root - a.d_star) <= 960 ? std::ldexp(1.0, a.l_root - a.d_star) : 0.0;
     a.wide = a.d_star > 31 ? 1 : 0;
     a.err = ds->err_dev;
-    const size_t smem = std::max<size_t>(4ull * g.cap + 8ull * g.ucap_s + 4ull * g.pcap_s + 2ull * g.cap,
-                                         dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 16 +
-                                                          (size_t)QT_WARPS * 32 * 16
-                                                    : 0);
-    e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int ctas_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_qt, QT_WARPS * 32, smem);
-    ctas_per_sm = std::max(1, ctas_per_sm);
-    // CTAs per SM slot over the launch (measured: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews
-    // batch); FT_OPT_QT_WAVES tunes it
-    const int waves = fti_opt(FT_OPT_QT_WAVES) > 0 ? (int)fti_opt(FT_OPT_QT_WAVES) : 8;
-    const int64_t target = (int64_t)148 * ctas_per_sm * waves;
-    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + nchunks - 1) / nchunks));
+    const int64_t target = (int64_t)148 * P.ctas_per_sm * waves;
+    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + P.nchunks - 1) / P.nchunks));
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
-    k_qt<<<dim3((unsigned)bx, (unsigned)nchunks), QT_WARPS * 32, smem, st>>>(a);
-    fti_count_launches(2);
+    k_qt<<<dim3((unsigned)bx, (unsigned)P.nchunks), QT_WARPS * 32, P.smem, st>>>(a);
+    fti_count_launches(1);
     return cudaGetLastError();
+}
+
+// CTAs per SM slot over a full scan (measured: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews
+// batch); FT_OPT_QT_WAVES tunes it
+int qt_waves() { return fti_opt(FT_OPT_QT_WAVES) > 0 ? (int)fti_opt(FT_OPT_QT_WAVES) : 8; }
+
+// flags [nq] from a row list {count, rows...}
+__global__ void k_rows_to_flags(const int* __restrict__ list, uint32_t* __restrict__ flag, int32_t nq) {
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) flag[i] = 0u;
+    __syncthreads();
+    const int c = list[0];
+    for (int i = threadIdx.x; i < c; i += blockDim.x) flag[list[1 + i]] = 1u;
+}
+
+}  // namespace
+
+cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq,
+                          const int64_t* d_docs, int64_t docs_ld, int64_t n_docs, double* d_out, int64_t out_ld,
+                          cudaStream_t st) {
+    (void)docs_ld;   // the Quadtree stage always scores one doc list shared by the batch
+    if (nq <= 0 || n_docs <= 0) return cudaSuccess;
+    QtPlan P;
+    cudaError_t e = qt_prepare(ds, L, d_qblock, nq, st, P);
+    if (e != cudaSuccess) return e;
+    return qt_scan(ds, P, nq, d_docs, n_docs, d_out, out_ld, QtArgs{}, qt_waves(), st);
+}
+
+// The prefilter (a3 + a4 fused): per query the m smallest (Quadtree value, doc id)
+// over all n docs, without writing the nq × n value matrix:
+//   1. scan a strided sample of n_s = n / 32 docs; per query the threshold t_q ≥ the sample's
+//      (r+1)-th smallest value (rounded up to FP32), r = E + 4√E + 8 with E = m·n_s/n the expected
+//      sample rank of the m-th key (so count(value ≤ t_q) ≥ m over all docs except with vanishing
+//      probability);
+//   2. scan all docs, appending every (value, doc) with value ≤ t_q to the query's list;
+//   3. select the m smallest (value, id) of each list (as a set: the Flowtree stage does not need
+//      them ordered).  Exact whenever m ≤ |list| ≤ capacity: every doc with a value ≤ the m-th key
+//      is listed;
+//   4. rows where that fails (list too short or overflowing — rare) are recomputed in full and
+//      selected as before (chunks and rows without such a query exit at once).
+// Falls back to the unfused pair (values written, then selected) when n < 32·m.
+cudaError_t fti_launch_prefilter(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, int64_t m,
+                                 int64_t* d_cand, double* d_cval, int* d_sel_scratch, cudaStream_t st) {
+    const int64_t n = ds->n;
+    cudaError_t e;
+    if (nq <= 0) return cudaSuccess;
+    const int64_t ns = n / 32;
+    if (n < 32 * m || fti_opt(FT_OPT_PREFILTER_UNFUSED) || ns < 1) {
+        if ((e = ds->s_vals.reserve(sizeof(double) * nq * n)) != cudaSuccess) return e;
+        if ((e = fti_launch_qt(ds, L, d_qblock, nq, nullptr, 0, n, ds->s_vals.as<double>(), n, st)) != cudaSuccess)
+            return e;
+        return fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m, d_cand, d_cval, m,
+                                 d_sel_scratch, st);
+    }
+    // the strided sample's doc ids, built once per dataset
+    if (ds->pf_ns != ns) {
+        std::vector<int64_t> h((size_t)ns);
+        for (int64_t i = 0; i < ns; i++) h[(size_t)i] = i * n / ns;
+        if ((e = ds->s_pf_samp.reserve(sizeof(int64_t) * ns)) != cudaSuccess) return e;
+        if ((e = cudaMemcpy(ds->s_pf_samp.p, h.data(), sizeof(int64_t) * ns, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return e;
+        ds->pf_ns = ns;
+    }
+    const double ex = (double)m * (double)ns / (double)n;
+    const int64_t r = std::min<int64_t>(ns - 1, (int64_t)std::ceil(ex + 4.0 * std::sqrt(ex) + 8.0));
+    const int64_t cap = FTI_PREFILTER_CAP;
+    if ((e = ds->s_pf_sval.reserve(sizeof(double) * nq * ns)) != cudaSuccess) return e;
+    if ((e = ds->s_pf_tval.reserve(sizeof(double) * nq)) != cudaSuccess) return e;
+    if ((e = ds->s_pf_cnt.reserve(sizeof(uint32_t) * nq)) != cudaSuccess) return e;
+    if ((e = ds->s_pf_cval.reserve(sizeof(double) * nq * cap)) != cudaSuccess) return e;
+    if ((e = ds->s_pf_cid.reserve(sizeof(int64_t) * nq * cap)) != cudaSuccess) return e;
+    if ((e = ds->s_pf_bad.reserve(sizeof(int) * ((size_t)nq + 1))) != cudaSuccess) return e;
+    if ((e = ds->s_pf_flag.reserve(sizeof(uint32_t) * nq)) != cudaSuccess) return e;
+    QtPlan P;
+    if ((e = qt_prepare(ds, L, d_qblock, nq, st, P)) != cudaSuccess) return e;
+    // 1. the sample and its per-query threshold
+    if ((e = qt_scan(ds, P, nq, ds->s_pf_samp.as<int64_t>(), ns, ds->s_pf_sval.as<double>(), ns, QtArgs{},
+                     std::max(1, qt_waves() / 4), st)) != cudaSuccess)
+        return e;
+    if ((e = fti_launch_row_threshold(ds->s_pf_sval.as<double>(), ns, ns, nq, r, ds->s_pf_tval.as<double>(), st)) !=
+        cudaSuccess)
+        return e;
+    // 2. every doc ≤ its query's threshold into the query's list
+    if ((e = cudaMemsetAsync(ds->s_pf_cnt.p, 0, sizeof(uint32_t) * nq, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ds->s_pf_bad.p, 0, sizeof(int), st)) != cudaSuccess) return e;
+    QtArgs tm{};
+    tm.thr = ds->s_pf_tval.as<double>();
+    tm.thr_ld = 1;
+    tm.ccnt = ds->s_pf_cnt.as<uint32_t>();
+    tm.cval = ds->s_pf_cval.as<double>();
+    tm.cid = ds->s_pf_cid.as<int64_t>();
+    tm.ccap = cap;
+    if ((e = qt_scan(ds, P, nq, nullptr, n, nullptr, 0, tm, qt_waves(), st)) != cudaSuccess) return e;
+    // 3. the m smallest of each list; rows whose list is short or overflowed are listed in pf_bad
+    if ((e = fti_launch_select(ds->s_pf_cval.as<double>(), cap, ds->s_pf_cid.as<int64_t>(), cap, cap, nq, (int32_t)m,
+                               d_cand, d_cval, m, d_sel_scratch, st, 0, ds->s_pf_cnt.as<uint32_t>(), nullptr, nullptr,
+                               ds->s_pf_bad.as<int>(), /*nosort=*/true)) != cudaSuccess)
+        return e;
+    // 4. those rows in full (every other CTA exits at once)
+    if ((e = ds->s_vals.reserve(sizeof(double) * nq * n)) != cudaSuccess) return e;
+    k_rows_to_flags<<<1, 1024, 0, st>>>(ds->s_pf_bad.as<int>(), ds->s_pf_flag.as<uint32_t>(), nq);
+    fti_count_launches(1);
+    QtArgs fb{};
+    fb.qflag = ds->s_pf_flag.as<uint32_t>();
+    if ((e = qt_scan(ds, P, nq, nullptr, n, ds->s_vals.as<double>(), n, fb, 1, st)) != cudaSuccess) return e;
+    return fti_launch_select(ds->s_vals.as<double>(), n, nullptr, 0, n, nq, (int32_t)m, d_cand, d_cval, m,
+                             d_sel_scratch, st, 0, nullptr, ds->s_pf_bad.as<int>() + 1, ds->s_pf_bad.as<int>());
 }

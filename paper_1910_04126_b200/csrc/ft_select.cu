@@ -146,16 +146,29 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
                                                      const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L,
                                                      int k, int64_t* __restrict__ out_ids,
                                                      double* __restrict__ out_val, int64_t out_ld,
-                                                     int* __restrict__ redo, int* __restrict__ nredo, int64_t id_base) {
+                                                     int* __restrict__ redo, int* __restrict__ nredo, int64_t id_base,
+                                                     const uint32_t* __restrict__ row_len, const int* __restrict__ rows_list,
+                                                     const int* __restrict__ nrows_list, int* __restrict__ bad,
+                                                     int nosort) {
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;                      // SEL_CAP
     uint32_t* bl = (uint32_t*)(sbuf + SEL_CAP);         // SEL_CAP
     __shared__ SelScratch sc;
     __shared__ int s_cnt, s_lt;
     __shared__ int s_wsum[16];
-    const int row = blockIdx.x;
+    if (rows_list && (int)blockIdx.x >= *nrows_list) return;
+    const int row = rows_list ? rows_list[blockIdx.x] : (int)blockIdx.x;
     const double* v = vals + (int64_t)row * vals_ld;
     const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
+    if (row_len) {
+        // a candidate list: rows shorter than k or longer than the list capacity are handed back
+        const int64_t len = (int64_t)row_len[row];
+        if (bad && (len > L || len < (int64_t)k)) {
+            if (threadIdx.x == 0) bad[1 + atomicAdd(bad, 1)] = row;
+            return;
+        }
+        L = min(L, len);
+    }
     const int kk = (int)min((int64_t)k, L);
     const int lane = threadIdx.x & 31;
     long long t0 = DBG ? clock64() : 0, t1 = 0, t2 = 0, t3 = 0;
@@ -300,7 +313,8 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
         if (threadIdx.x == 0) redo[atomicAdd(nredo, 1)] = row;
         return;
     }
-    if (cnt > 2048 && cnt > kk && kk > 0) {    // small sets sort faster than they rank-select
+    // small sets sort faster than they rank-select — unless only the set is wanted (nosort)
+    if ((cnt > 2048 || nosort) && cnt > kk && kk > 0) {
         // the kk-th smallest gathered (key, id) — composites are distinct — then keep the kk keys
         // at or below it (positions by warp-aggregated atomics: the sort below fixes the order)
         unsigned long long th;
@@ -335,10 +349,12 @@ __global__ void __launch_bounds__(512, 2) k_select_fast(const double* __restrict
         __syncthreads();
         nk = kk;
     }
-    const int P = fti_pow2_at_least(max(nk, 2));
-    for (int i = nk + threadIdx.x; i < P; i += blockDim.x) { bh[i] = ~0ull; bl[i] = 0xFFFFFFFFu; }
-    __syncthreads();
-    sort_pairs(bh, bl, P);
+    if (!nosort) {
+        const int P = fti_pow2_at_least(max(nk, 2));
+        for (int i = nk + threadIdx.x; i < P; i += blockDim.x) { bh[i] = ~0ull; bl[i] = 0xFFFFFFFFu; }
+        __syncthreads();
+        sort_pairs(bh, bl, P);
+    }
     if (DBG) t3 = clock64();
     for (int t = threadIdx.x; t < k; t += blockDim.x) {
         int64_t oid = -1;
@@ -365,7 +381,8 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
                                                 const int64_t* __restrict__ ids, int64_t ids_ld, int64_t L, int k,
                                                 int64_t* __restrict__ out_ids, double* __restrict__ out_val,
                                                 int64_t out_ld, int P, const int* __restrict__ rows_list,
-                                                const int* __restrict__ nrows_list, int64_t id_base) {
+                                                const int* __restrict__ nrows_list, int64_t id_base,
+                                                const uint32_t* __restrict__ row_len) {
     if (rows_list && (int)blockIdx.x >= *nrows_list) return;
     extern __shared__ unsigned long long sbuf[];
     unsigned long long* bh = sbuf;               // P
@@ -377,6 +394,7 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
     const int row = rows_list ? rows_list[blockIdx.x] : blockIdx.x;
     const double* v = vals + (int64_t)row * vals_ld;
     const int64_t* id = ids ? ids + (int64_t)row * ids_ld : nullptr;
+    if (row_len) L = std::min<int64_t>(L, (int64_t)row_len[row]);
     const int kk = (int)std::min<int64_t>(k, L);
     if (threadIdx.x == 0) { s_ph = 0; s_mh = 0; s_pl = 0; s_ml = 0; s_need = kk; s_done = 0; s_cnt = 0; }
     __syncthreads();
@@ -462,11 +480,67 @@ __global__ void __launch_bounds__(512) k_select(const double* __restrict__ vals,
     }
 }
 
+// Per row, a value t ≥ the r-th smallest (0-based) of the row's L values and within FP32 rounding of
+// it: the values rounded up to FP32 (order-preserving u32 keys, NaN largest), the r-th key by MSD
+// radix select with 11/11/10-bit digits (three passes over the row through L2).  The prefilter's
+// sample threshold (only count(value ≤ t) ≥ m matters there, so the FP32 round-up is harmless).
+__global__ void __launch_bounds__(256) k_row_threshold(const double* __restrict__ vals, int64_t ld, int64_t L, int64_t r,
+                                                       double* __restrict__ thr) {
+    __shared__ unsigned hist[2048];
+    __shared__ uint32_t s_pre, s_need;
+    const int row = blockIdx.x;
+    const double* v = vals + (int64_t)row * ld;
+    auto key_of = [](double x) -> uint32_t {
+        if (x != x) return 0xFFFFFFFFu;
+        const uint32_t b = __float_as_uint(__double2float_ru(x));
+        return (b >> 31) ? ~b : (b | 0x80000000u);
+    };
+    if (threadIdx.x == 0) { s_pre = 0u; s_need = (uint32_t)r; }
+    const int shift[3] = {21, 10, 0}, width[3] = {11, 11, 10};
+    uint32_t pmask = 0u;
+    for (int p = 0; p < 3; p++) {
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0u;
+        __syncthreads();
+        const uint32_t pre = s_pre;
+        const uint32_t dm = (1u << width[p]) - 1u;
+        for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+            const uint32_t k = key_of(v[i]);
+            if ((k & pmask) == pre) atomicAdd(&hist[(k >> shift[p]) & dm], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t need = s_need, cum = 0u, b = 0u;
+            for (; b < dm; b++) {
+                if (cum + hist[b] > need) break;
+                cum += hist[b];
+            }
+            s_need = need - cum;
+            s_pre = pre | (b << shift[p]);
+        }
+        pmask |= dm << shift[p];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t k = s_pre;
+        const uint32_t b = (k >> 31) ? (k & 0x7FFFFFFFu) : ~k;
+        thr[row] = k == 0xFFFFFFFFu ? __longlong_as_double(0x7ff0000000000000ll) : (double)__uint_as_float(b);
+    }
+}
+
 }  // namespace
+
+cudaError_t fti_launch_row_threshold(const double* d_vals, int64_t ld, int64_t L, int32_t rows, int64_t r,
+                                     double* d_thr, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    k_row_threshold<<<rows, 256, 0, st>>>(d_vals, ld, L, r, d_thr);
+    fti_count_launches(1);
+    return cudaGetLastError();
+}
 
 cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64_t* d_ids, int64_t ids_ld, int64_t L,
                               int32_t rows, int32_t k, int64_t* d_out_ids, double* d_out_val, int64_t out_ld,
-                              int* d_scratch, cudaStream_t st, int64_t id_base) {
+                              int* d_scratch, cudaStream_t st, int64_t id_base, const uint32_t* d_row_len,
+                              const int* d_rows_list, const int* d_nrows_list, int* d_bad, bool nosort) {
     if (rows <= 0) return cudaSuccess;
     int kk = (int)std::min<int64_t>(k, L);
     int P = fti_pow2_at_least(std::max(kk, 2));
@@ -475,7 +549,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     if (e != cudaSuccess) return e;
     if (fti_opt(FT_OPT_SELECT_RADIX)) {   // test option: the radix kernel for every row
         k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P,
-                                          nullptr, nullptr, id_base);
+                                          d_rows_list, d_nrows_list, id_base, d_row_len);
         fti_count_launches(1);
         return cudaGetLastError();
     }
@@ -494,7 +568,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     kf<<<rows, 512, smem_f, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, redo, nredo,
-                                  id_base);
+                                  id_base, d_row_len, d_rows_list, d_nrows_list, d_bad, nosort ? 1 : 0);
     if (dbg) {
         unsigned long long h[8];
         cudaStreamSynchronize(st);
@@ -507,7 +581,7 @@ cudaError_t fti_launch_select(const double* d_vals, int64_t vals_ld, const int64
     }
     // pass 2: MSD radix selection of the listed rows (CTAs past the list exit at once)
     k_select<<<rows, 512, smem, st>>>(d_vals, vals_ld, d_ids, ids_ld, L, k, d_out_ids, d_out_val, out_ld, P, redo,
-                                      nredo, id_base);
+                                      nredo, id_base, d_row_len);
     fti_count_launches(2);
     return cudaGetLastError();
 }

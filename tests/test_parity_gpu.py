@@ -484,13 +484,19 @@ def test_knn_tiny(ft, prefilter_m):
         assert_ft_close(vals[q], [ftv[i] for i in ids[q]])
 
 
-@pytest.mark.parametrize("n_docs,radix", [(5000, False), (20000, False), (20000, True)])
-def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix):
+@pytest.mark.parametrize("n_docs,radix,unfused", [(5000, False, False), (20000, False, False), (20000, True, False),
+                                                   (20000, False, True)])
+def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix, unfused):
     """With k = m the returned set is exactly the Quadtree top-m (bit-exact keys, ties by id),
-    ordered by (Flowtree value, id) as the oracle ranks it.  n ≤ 8192 sorts the whole row; n = 20000 takes the sample-threshold path (the Quadtree
-    values at d = 300 are heavily tied); FT_OPT_SELECT_RADIX forces the MSD radix kernel."""
+    ordered by (Flowtree value, id) as the oracle ranks it.  n = 5000 < 32·m runs the unfused
+    prefilter (values written, whole rows sorted); n = 20000 the fused sample-threshold scan with
+    candidate lists (the Quadtree values at d = 300 are heavily tied), or with
+    FT_OPT_PREFILTER_UNFUSED the row selection's sample-threshold path; FT_OPT_SELECT_RADIX forces
+    the MSD radix kernel."""
     if radix:
         opt("FT_OPT_SELECT_RADIX")
+    if unfused:
+        opt("FT_OPT_PREFILTER_UNFUSED")
     wl = get_workload("reviews", n_docs=n_docs, n_queries=4)
     T = oracle_tree(wl)
     ix, ds = _setup(ft, wl)
@@ -506,6 +512,35 @@ def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix):
         assert_topk_tieband(ids[q], vals[q], top, ftv, m, what=f"prefilter q{q}")
         v = vals[q]
         assert np.all((v[1:] > v[:-1]) | ((v[1:] == v[:-1]) & (ids[q][1:] > ids[q][:-1])))
+
+
+def test_prefilter_fused_overflow_fallback(ft):
+    """Fused prefilter rows whose candidate list overflows: 36,000 copies of one doc plus 2,000
+    others (n = 38,000 ≥ 32·m), query 0 = that doc, so 36,000 docs tie at Quadtree value 0 and the
+    list (capacity 32,768) overflows — the row is recomputed in full and selected with ties by id.
+    Query 1 is an ordinary query (the list path).  Both must equal the oracle's (value, id) top-m."""
+    base = get_workload("reviews", n_docs=2001, n_queries=2)
+    T = oracle_tree(base)
+    src = [0] * 36000 + list(range(1, 2001))
+    docs = [base.doc(d) for d in src]
+    doc_off = np.zeros(len(src) + 1, np.int64)
+    doc_off[1:] = np.cumsum([len(i) for i, _ in docs])
+    ids = np.concatenate([i for i, _ in docs]).astype(np.int32)
+    w = np.concatenate([x for _, x in docs]).astype(np.uint32)
+    d0i, d0w = base.doc(0)
+    q1i, q1w = base.query(1)
+    q_off = np.array([0, len(d0i), len(d0i) + len(q1i)], np.int64)
+    q_ids = np.concatenate([d0i, q1i]).astype(np.int32)
+    q_w = np.concatenate([d0w, q1w]).astype(np.uint32)
+    ix = ft.Index(base.X, seed=base.tree_seed, max_depth=base.max_depth)
+    ds = ft.Dataset(ix, doc_off, ids, w)
+    m = 300
+    got, vals = ds.knn(q_off, q_ids, q_w, m, m)
+    for q, (b, bw) in enumerate([(d0i, d0w), (q1i, q1w)]):
+        qd = pmap(lambda d: T.qt(*base.doc(d), b, bw)[1], range(2001))
+        top = sorted(range(len(src)), key=lambda i: (qd[src[i]], i))[:m]
+        assert set(got[q].tolist()) == set(top), f"query {q}"
+    assert set(got[0].tolist()) == set(range(m))        # the tied copies, smallest ids first
 
 
 def test_knn_padding_and_errors(ft):

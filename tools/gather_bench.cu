@@ -65,6 +65,46 @@ __global__ void __launch_bounds__(256, 1) k_gather(const int8_t* __restrict__ X,
                 d[1] = make_uint4(v[u][4], v[u][5], v[u][6], v[u][7]);
             }
             __syncthreads();
+        } else if (MODE == 3) {
+            // LDG with CH units of 32 B per thread in flight (threads beyond the tile's units idle)
+            constexpr int U = CH;
+            const int units = TM * ROW / 32;
+            for (int g0 = 0; g0 < units; g0 += U * blockDim.x) {
+                uint32_t v[U][8];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int g = g0 + u * blockDim.x + t;
+                    if (g < units) {
+                        const int r = g / (ROW / 32), c = g % (ROW / 32);
+                        asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                     : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3]), "=r"(v[u][4]),
+                                       "=r"(v[u][5]), "=r"(v[u][6]), "=r"(v[u][7])
+                                     : "l"(X + (size_t)tr[r] * ROW + 32 * c));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int g = g0 + u * blockDim.x + t;
+                    if (g < units) {
+                        uint4* d = (uint4*)(sm + (size_t)g * 32);
+                        d[0] = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+                        d[1] = make_uint4(v[u][4], v[u][5], v[u][6], v[u][7]);
+                    }
+                }
+            }
+            __syncthreads();
+        } else if (MODE == 4) {
+            // cp.async rolling: tile it issued, then wait for tile it − 1 (two tiles in flight, 60 KB
+            // halves of the ring per tile: rows of 480 B)
+            const int half = it & 1;
+            for (int g = t; g < TM * ROW / 32; g += blockDim.x) {
+                const int r = g / (ROW / 32), c = g % (ROW / 32);
+                const int8_t* src = X + (size_t)tr[r] * ROW + 16 * c;   // first half of each row only
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(sm + half * (RING / 2) + (size_t)g * 16)), "l"(src) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
         } else {
             // bulk copies of CH bytes: 128 × 960 / CH requests spread over the threads
             constexpr int NREQ = TM * ROW / CH;
@@ -105,7 +145,7 @@ void run(const char* name, const int8_t* X, const int32_t* rows, int tiles, unsi
     cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
-    const double bytes = 3.0 * 148 * tiles * TM * (double)ROW;
+    const double bytes = 3.0 * 148 * tiles * TM * (double)ROW / (MODE == 4 ? 2 : 1);
     printf("%-28s %8.3f ms  %7.2f TB/s useful  err=%s\n", name, ms / 3, bytes / (ms / 1e3) / 1e12,
            cudaGetErrorString(cudaGetLastError()));
 }
@@ -129,5 +169,10 @@ int main() {
     run<2, 192>("bulk 192B", X, rows, tiles, sink);
     run<2, 960>("bulk 960B", X, rows, tiles, sink);
     run<2, 32>("bulk 32B", X, rows, tiles, sink);
+    run<3, 2>("ldg 2 units/thread (16 KB)", X, rows, tiles, sink);
+    run<3, 4>("ldg 4 units/thread (32 KB)", X, rows, tiles, sink);
+    run<3, 8>("ldg 8 units/thread (64 KB)", X, rows, tiles, sink);
+    run<3, 15>("ldg 15 units/thread (120 KB)", X, rows, tiles, sink);
+    run<4, 16>("cp.async rolling 2x60KB (half rows)", X, rows, tiles, sink);
     return 0;
 }

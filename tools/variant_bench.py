@@ -11,7 +11,16 @@ CHILD = r'''
 import os, sys, json, numpy as np, torch
 sys.path.insert(0, ROOT)
 from paper_1910_04126_b200 import flowtree as ft, workloads
-wl = workloads.make(CFG, n_queries=NQ)
+cfg, _, trunc = CFG.partition(":q")
+wl = workloads.make(cfg, n_queries=NQ)
+if trunc:   # "reviews:q48": every query cut to its first 48 items (supports ≤ 48)
+    T = int(trunc)
+    qs = [wl.query(j) for j in range(wl.nq)]
+    qs = [(i[:T], x[:T]) for i, x in qs]
+    q_off = np.zeros(len(qs) + 1, np.int64); q_off[1:] = np.cumsum([len(i) for i, _ in qs])
+    import dataclasses
+    wl = dataclasses.replace(wl, q_off=q_off, q_ids=np.concatenate([i for i, _ in qs]).astype(np.int32),
+                             q_w=np.concatenate([x for _, x in qs]).astype(np.uint32))
 ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
 ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
 qi = torch.from_numpy(wl.q_ids).cuda(); qw = torch.from_numpy(wl.q_w.view(np.int32)).cuda().view(torch.uint32)
@@ -36,7 +45,7 @@ def main():
     for name in names:
         lib = os.path.join(ROOT, "paper_1910_04126_b200", "libflowtree_b200.so") if name == "main" else \
             os.path.join(ROOT, "build", "variants", name, "libflowtree_b200.so")
-        out = f"/tmp/vb_{cfg}_{name}"
+        out = f"/tmp/vb_{cfg.replace(':', '_')}_{name}"
         code = CHILD.replace("ROOT", repr(ROOT)).replace("CFG", repr(cfg)).replace("NQ", str(nq)).replace("OUT", repr(out))
         env = dict(os.environ, FT_LIB=lib)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
