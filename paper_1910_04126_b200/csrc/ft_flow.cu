@@ -62,9 +62,20 @@ struct FtArgs {
     int32_t q0;                  // first query of this launch (grid.y ≤ 65535)
 };
 
+#ifndef FT_BATCH_B
+#define FT_BATCH_B 1       // phase B batched per depth (0: one warp northwest corner per node)
+#endif
 constexpr int64_t FT_BITMAP_MAX_N = 1 << 19;   // 16K words: 64 KB bitmap + 64 KB rank at most
 
 constexpr int FT_WARPS = 8;                 // warps per CTA (fewer when the supports are large)
+
+// per-warp shared words: dvoc, dres, dcum [Sd]; qres, qcum [Sq]; batched phase B: node table
+// [8][32], u16 lists [Sd], [Sq], u8 node indices [Sd], [Sq]
+__host__ __device__ __forceinline__ int ft_per_warp_words(int Sd, int Sq) {
+    const int b16 = 2 * ((Sd + 1) & ~1) + 2 * ((Sq + 1) & ~1);
+    const int b8 = ((Sd + 3) & ~3) + ((Sq + 3) & ~3);
+    return 3 * Sd + 2 * Sq + 256 + (b16 + b8 + 3) / 4;
+}
 constexpr size_t FT_SMEM_MAX = 227 * 1024;
 
 struct PairCtx {
@@ -77,9 +88,18 @@ struct PairCtx {
     uint32_t* dcum;
     uint32_t* qres;
     uint32_t* qcum;
+    // batched phase B (one depth's common M-nodes at a time): concatenated item lists, their node
+    // index in the batch, and per-node {doc start, query start, doc len, query len, doc base, query
+    // base, T, node id}
+    uint16_t* alst;
+    uint16_t* blst;
+    uint8_t* aseg;
+    uint8_t* bseg;
+    uint32_t* nb;           // [8][32]
     const float* trow_base; // table for this query or null
     uint32_t tld;           // its row pitch
     const uint2* map;       // candidate-vocabulary bitmap {bits, rank} per 32 ids, or null (row = vocab)
+    const uint16_t* gml;    // the query's M-node item lists
 };
 
 __device__ __forceinline__ float pair_dist(const PairCtx& c, uint32_t x, uint32_t y, int jq) {
@@ -187,6 +207,129 @@ __device__ void nw_corner(const PairCtx& c, const uint16_t* a_list, int la, cons
     for (int p = lane; p < lb; p += 32) {
         const uint32_t hi = c.qcum[p], lo = p ? c.qcum[p - 1] : 0u;
         c.qres[b_list ? b_list[p] : p] = hi <= T ? 0u : hi - (lo > T ? lo : T);
+    }
+    __syncwarp();
+}
+
+// Phase B batched over the common M-nodes of ONE depth (≤ 32 records of the doc, lane l holds record
+// l): the nodes are disjoint subtrees, so their northwest corners are independent (reading R11) and
+// run as one segmented pass — the lists concatenated, one warp scan per side, per node
+// T = min(totals), every doc item emitting its overlaps with the query items of its own node, the
+// leftovers written back — instead of a warp pass per node.  The triples are those of nw_corner
+// node by node.
+template <bool EXPORT>
+__device__ void batch_nw(const PairCtx& c, const uint4& rec, const uint4& qe, bool hit, int lane, double& cost) {
+    const unsigned hm = __ballot_sync(0xffffffffu, hit);
+    if (!hm) return;
+    const int nh = __popc(hm);
+    uint32_t* nDS = c.nb;
+    uint32_t* nQS = c.nb + 32;
+    uint32_t* nDL = c.nb + 64;
+    uint32_t* nQL = c.nb + 96;
+    uint32_t* nBA = c.nb + 128;
+    uint32_t* nBB = c.nb + 160;
+    uint32_t* nT = c.nb + 192;
+    uint32_t* nID = c.nb + 224;
+    const uint32_t dl = hit ? rec.z : 0u, ql = hit ? qe.z : 0u;
+    const uint32_t dsi = fti_warp_incl_u32(dl, lane), qsi = fti_warp_incl_u32(ql, lane);
+    const int LA = (int)__shfl_sync(0xffffffffu, dsi, 31), LB = (int)__shfl_sync(0xffffffffu, qsi, 31);
+    const int ni = __popc(hm & ((1u << lane) - 1u));
+    if (hit) {
+        nDS[ni] = dsi - dl; nQS[ni] = qsi - ql; nDL[ni] = dl; nQL[ni] = ql;
+    }
+    // the concatenated lists (u16 item indices) and each element's node: element p of a side finds
+    // its node by binary search over the node starts
+    uint32_t* nDO = c.nb + 192;   // list offsets (nT / nID slots, rewritten below)
+    uint32_t* nQO = c.nb + 224;
+    if (hit) { nDO[ni] = rec.y; nQO[ni] = qe.y; }
+    __syncwarp();
+    auto seg_of = [&](const uint32_t* starts, int p) {
+        int lo = 0, hi = nh - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (starts[mid] <= (uint32_t)p) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    for (int p = lane; p < LA; p += 32) {
+        const int i = seg_of(nDS, p);
+        c.alst[p] = c.a->mlists[nDO[i] + ((uint32_t)p - nDS[i])];
+        c.aseg[p] = (uint8_t)i;
+    }
+    for (int p = lane; p < LB; p += 32) {
+        const int i = seg_of(nQS, p);
+        c.blst[p] = c.gml[nQO[i] + ((uint32_t)p - nQS[i])];
+        c.bseg[p] = (uint8_t)i;
+    }
+    __syncwarp();
+    if (hit) nID[ni] = rec.x;
+    // global inclusive prefix sums over the concatenations
+    uint32_t carry = 0;
+    for (int p0 = 0; p0 < LA; p0 += 32) {
+        const int p = p0 + lane;
+        const uint32_t v = p < LA ? c.dres[c.alst[p]] : 0u;
+        const uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < LA) c.dcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    carry = 0;
+    for (int p0 = 0; p0 < LB; p0 += 32) {
+        const int p = p0 + lane;
+        const uint32_t v = p < LB ? c.qres[c.blst[p]] : 0u;
+        const uint32_t incl = fti_warp_incl_u32(v, lane) + carry;
+        if (p < LB) c.qcum[p] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    if (lane < nh) {   // per node: bases and T = min of the two totals under it
+        const uint32_t ds = nDS[lane], qs = nQS[lane];
+        const uint32_t ba = ds ? c.dcum[ds - 1] : 0u, bb = qs ? c.qcum[qs - 1] : 0u;
+        const uint32_t ta = c.dcum[ds + nDL[lane] - 1] - ba, tb = c.qcum[qs + nQL[lane] - 1] - bb;
+        nBA[lane] = ba; nBB[lane] = bb; nT[lane] = ta < tb ? ta : tb;
+    }
+    __syncwarp();
+    for (int p = lane; p < LA; p += 32) {
+        const int i = c.aseg[p];
+        const uint32_t ba = nBA[i], T = nT[i], ds = nDS[i];
+        const uint32_t hi_a = c.dcum[p] - ba;
+        const uint32_t lo_a = (uint32_t)p > ds ? c.dcum[p - 1] - ba : 0u;
+        const uint32_t end = hi_a < T ? hi_a : T;
+        if (lo_a >= end) continue;
+        const uint32_t bb = nBB[i], qs = nQS[i];
+        int lo = (int)qs, hi = (int)(qs + nQL[i]);
+        while (lo < hi) {   // first j of the node's query items with cum > lo_a
+            const int mid = (lo + hi) >> 1;
+            if (c.qcum[mid] - bb > lo_a) hi = mid; else lo = mid + 1;
+        }
+        const uint32_t x = c.dvoc[c.alst[p]] & FTI_VOCAB_MASK;
+        const int jend = (int)(qs + nQL[i]);
+        for (int j = lo; j < jend; j++) {
+            const uint32_t lo_b = (uint32_t)j > qs ? c.qcum[j - 1] - bb : 0u;
+            if (lo_b >= end) break;
+            const uint32_t hi_b = c.qcum[j] - bb;
+            const uint32_t s0 = lo_b > lo_a ? lo_b : lo_a;
+            const uint32_t s1 = hi_b < end ? hi_b : end;
+            if (s1 > s0) {
+                const uint32_t eta = s1 - s0;
+                const int jq = c.blst[j];
+                const uint32_t y = c.qitem[jq].x & FTI_VOCAB_MASK;
+                if (x != y) cost += (double)eta * (double)pair_dist(c, x, y, jq);
+                emit<EXPORT>(*c.a, x, y, eta, nID[i]);
+            }
+        }
+    }
+    __syncwarp();
+    for (int p = lane; p < LA; p += 32) {
+        const int i = c.aseg[p];
+        const uint32_t ba = nBA[i], T = nT[i];
+        const uint32_t hi = c.dcum[p] - ba, lo = (uint32_t)p > nDS[i] ? c.dcum[p - 1] - ba : 0u;
+        c.dres[c.alst[p]] = hi <= T ? 0u : hi - (lo > T ? lo : T);
+    }
+    for (int p = lane; p < LB; p += 32) {
+        const int i = c.bseg[p];
+        const uint32_t bb = nBB[i], T = nT[i];
+        const uint32_t hi = c.qcum[p] - bb, lo = (uint32_t)p > nQS[i] ? c.qcum[p - 1] - bb : 0u;
+        c.qres[c.blst[p]] = hi <= T ? 0u : hi - (lo > T ? lo : T);
     }
     __syncwarp();
 }
@@ -314,7 +457,7 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     float* Y = a.use_bitmap ? (float*)(rank + a.nwords) : (float*)(vh + a.L.vh_cap);
     uint32_t* wbase = (uint32_t*)(Y + (a.small_d ? a.Sq * a.d : 0));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int per_warp = 3 * a.Sd + 2 * a.Sq;
+    const int per_warp = ft_per_warp_words(a.Sd, a.Sq);
     uint32_t* wsm = wbase + warp * per_warp;
 
     const uint32_t sq = hdr->s, U = hdr->U, vh_mask = hdr->vh_mask, mh_mask = hdr->mh_mask;
@@ -364,6 +507,12 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
     c.dcum = wsm + 2 * a.Sd;
     c.qres = wsm + 3 * a.Sd;
     c.qcum = wsm + 3 * a.Sd + a.Sq;
+    c.nb = wsm + 3 * a.Sd + 2 * a.Sq;
+    c.alst = (uint16_t*)(c.nb + 256);
+    c.blst = c.alst + ((a.Sd + 1) & ~1);
+    c.aseg = (uint8_t*)(c.blst + ((a.Sq + 1) & ~1));
+    c.bseg = c.aseg + ((a.Sd + 3) & ~3);
+    c.gml = (const uint16_t*)(slot + a.L.off_ml);
     c.trow_base = a.tab.table ? a.tab.table + a.tab.row_base[q] : nullptr;
     c.tld = a.tab.table ? (uint32_t)a.tab.pitch[q] : 0u;
     c.map = a.tab.map ? a.tab.map + (int64_t)q * ((a.N + 31) / 32) : nullptr;
@@ -431,12 +580,16 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
         // ---- phase B: common M-nodes, deepest first ----
         const uint32_t m0 = a.mn_off[doc], m1 = a.mn_off[doc + 1];
         if (m1 > m0 && hdr->n_mn > 0) {
-            for (uint32_t cb = m0; cb < m1; cb += 32) {
+            // records are ordered (depth desc, node asc): chunks of ≤ 32 records of one depth
+            uint32_t cb = m0;
+            while (cb < m1) {
                 const uint32_t r = cb + lane;
-                uint4 rec = make_uint4(0, 0, 0, 0), qe = make_uint4(0, 0, 0, 0);
+                uint4 rec = make_uint4(0, 0, 0, 0xFFFFFFFFu), qe = make_uint4(0, 0, 0, 0);
+                if (r < m1) rec = a.mnodes[r];
+                const uint32_t dep0 = __shfl_sync(0xffffffffu, rec.w, 0);
+                const int nrec = __popc(__ballot_sync(0xffffffffu, r < m1 && rec.w == dep0));
                 bool hit = false;
-                if (r < m1) {
-                    rec = a.mnodes[r];
+                if (lane < nrec) {
                     uint32_t h = fti_hash(rec.x) & mh_mask;
                     while (true) {
                         const uint4 e = gmh[h];
@@ -445,17 +598,22 @@ __global__ void __launch_bounds__(FT_WARPS * 32, 4) k_flowtree(FtArgs a) {
                         h = (h + 1) & mh_mask;
                     }
                 }
-                unsigned hm = __ballot_sync(0xffffffffu, hit);
-                while (hm) {
-                    const int l = __ffs(hm) - 1;
-                    hm &= hm - 1;
-                    const uint32_t node = __shfl_sync(0xffffffffu, rec.x, l);
-                    const uint32_t dlo = __shfl_sync(0xffffffffu, rec.y, l);
-                    const uint32_t dln = __shfl_sync(0xffffffffu, rec.z, l);
-                    const uint32_t qlo = __shfl_sync(0xffffffffu, qe.y, l);
-                    const uint32_t qln = __shfl_sync(0xffffffffu, qe.z, l);
-                    nw_corner<EXPORT>(c, a.mlists + dlo, (int)dln, gml + qlo, (int)qln, node, lane, cost);
+                if (FT_BATCH_B) {
+                    batch_nw<EXPORT>(c, rec, qe, hit, lane, cost);
+                } else {
+                    unsigned hm = __ballot_sync(0xffffffffu, hit);
+                    while (hm) {
+                        const int l = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        const uint32_t node = __shfl_sync(0xffffffffu, rec.x, l);
+                        const uint32_t dlo = __shfl_sync(0xffffffffu, rec.y, l);
+                        const uint32_t dln = __shfl_sync(0xffffffffu, rec.z, l);
+                        const uint32_t qlo = __shfl_sync(0xffffffffu, qe.y, l);
+                        const uint32_t qln = __shfl_sync(0xffffffffu, qe.z, l);
+                        nw_corner<EXPORT>(c, a.mlists + dlo, (int)dln, gml + qlo, (int)qln, node, lane, cost);
+                    }
                 }
+                cb += (uint32_t)nrec;
             }
         }
         // ---- phase C: the root ----
@@ -503,7 +661,7 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
     const size_t ysm = a.small_d ? (size_t)a.Sq * a.d * 4 : 0;
     // per-warp residual arrays: fewer warps per CTA when large supports would exceed the
     // shared-memory limit (227 KB); FT_ERANGE-class failure when even one warp does not fit
-    const size_t per_warp = (size_t)(3 * a.Sd + 2 * a.Sq) * 4;
+    const size_t per_warp = (size_t)ft_per_warp_words(a.Sd, a.Sq) * 4;
     const size_t fixed = (size_t)a.Sq * 8 + lookup + ysm;
     int warps = FT_WARPS;
     while (warps > 1 && fixed + warps * per_warp > FT_SMEM_MAX) warps--;
