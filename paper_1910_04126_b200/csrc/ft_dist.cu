@@ -240,6 +240,7 @@ struct DistArgs {
     const int64_t* row_base;    // [nq] ELEMENT offset of each query's table
     const int32_t* pitch;       // [nq] per-query row pitch (floats)
     float* table;
+    int kz;                     // K bytes from kz on are zero padding in every row (round_up(d, 16))
     int nstage;                 // A ring depth
     int blk_outer;              // the ring holds a tile's whole K range (nstage == nks)
 };
@@ -299,6 +300,20 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // with the ring slot of K stage c fixed (nstage == nks), the all-zero K granules of the padding
+    // (K ≥ round_up(d, 16)) are zeroed once here and never copied
+    const bool kfixed = NSTAGE == a.nks;
+    if (kfixed && a.kz < a.kpad) {
+        const int gz0 = a.kz / 16, gz1 = a.kpad / 16;   // dead 16-byte K granules [gz0, gz1)
+        const int per = (gz1 - gz0) * TM * NL;
+        for (int e = t; e < per; e += blockDim.x) {
+            const int g = gz0 + e % (gz1 - gz0), rest = e / (gz1 - gz0);
+            const int r = rest % TM, p = rest / TM;
+            const int c = g / (KS / 16), kb = (g % (KS / 16)) * 16;
+            *(uint4*)(aring + (size_t)c * STAGE_BYTES + p * STAGE_LIMB + cm_off(r, kb, SBO_A)) = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -426,11 +441,12 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
             for (int c = 0; c < a.nks; c++) {
                 if (!first) TW(0, mbar_wait(&empty[s], eph));
                 const uint32_t st = abase + (uint32_t)s * STAGE_BYTES;
+                const bool live = !kfixed || KS * c + 16 * gq < a.kz;   // not an all-zero padding granule
 #pragma unroll
                 for (int p = 0; p < NL; p++)
 #pragma unroll
                     for (int rg = 0; rg < RG; rg++)
-                        if (grp_ok(rg) && !(FTD_ABL & 1)) {
+                        if (grp_ok(rg) && live && !(FTD_ABL & 1)) {
                             if (FTD_L2POL) cp_async16_pol(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS, pol);
                             else cp_async16(st + p * STAGE_LIMB + doff[rg], src[rg] + (size_t)c * ROWB + p * KS);
                         }
@@ -1007,6 +1023,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.N = ix->N;
     a.nks = ix->nks;
     a.kpad = ix->nks * KS;
+    a.kz = std::min(a.kpad, (ix->d + 15) & ~15);
     a.scale = (float)std::ldexp(1.0, -ix->qexp);
     a.qblock = d_qblock;
     a.L = L;

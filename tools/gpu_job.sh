@@ -1,4 +1,4 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_parity_gpu.py -x -q -k "tiny or subsets or vocab_hash or capped or degenerate or image or chunked" > gpurun_out/pytest_b2.log 2>&1; echo "rc $?" >> gpurun_out/pytest_b2.log
-python tools/variant_bench.py image 200 main nob > gpurun_out/vb_img2.log 2>&1
+python -m pytest tests/test_parity_gpu.py -x -q -k "distance or subsets or full_size" > gpurun_out/pytest_kz.log 2>&1; echo "rc $?" >> gpurun_out/pytest_kz.log
+python tools/variant_bench.py reviews 1000 prev main > gpurun_out/vb_kz.log 2>&1
