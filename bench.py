@@ -327,7 +327,8 @@ def run_b200(args):
     qt_bytes = Q * (8 * n_qt + 16 * ds.n)
     alg_bytes = {"quadtree": qt_bytes * stages["quadtree"][1], "dist_table": units["dist_table"],
                  "flowtree": units["flowtree"]}
-    kern = {"quadtree": "k_qt (Quadtree estimate, a3)",
+    kern = {"quadtree": "k_qt (Quadtree estimate, a3) in the fused prefilter (a3+a4: 1/32-sample scan, "
+                        "threshold scan appending candidates, list top-m; the stage time includes the selection)",
             "dist_table": "k_dist_i8 (tcgen05 kind::i8 exact distance table, a5)",
             "flowtree": "k_ftd (lane-per-pair Flowtree estimate, a6) + k_flowtree (list mode: pairs sharing an M-node)"}
     traffic_all = {}

@@ -8,14 +8,10 @@ $B > gpurun_out/bench_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B \
   > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
-Q="python tools/kprof.py qt --queries 1000 --reps 1"
-$Q > gpurun_out/kp_qt.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_qt$" -c 1 -o gpurun_out/prof_qt $Q \
-  > gpurun_out/ncu_qt.log 2>&1
-echo "qt rc=$?"
 K="python tools/kprof.py knn --queries 1000 --reps 1"
 $K > gpurun_out/kp_knn.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_dist_i8|k_ftd|k_flowtree|k_select_fast|k_vocab|k_qt_dense|k_tiles|k_dist_prep|k_tile_plan" -c 9 \
+  ncu --set full --clock-control none --import-source on \
+  -k regex:"k_qt$|k_row_threshold|k_select_fast|k_dist_i8|k_ftd|k_flowtree|k_vocab|k_tiles|k_dist_prep" -c 16 \
   -o gpurun_out/prof_knn $K > gpurun_out/ncu_knn.log 2>&1
 echo "knn rc=$?"
 X="python tools/kprof.py ft --queries 64 --reps 1"
@@ -23,6 +19,11 @@ $X > gpurun_out/kp_ftd.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_ftd|k_flowtree" -c 2 -o gpurun_out/prof_ftd $X \
   > gpurun_out/ncu_ftd.log 2>&1
 echo "ftd rc=$?"
+I="python tools/kprof.py ft --config image --queries 16 --reps 1"
+$I > gpurun_out/kp_img.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_flowtree" -c 1 -o gpurun_out/prof_img $I \
+  > gpurun_out/ncu_img.log 2>&1
+echo "img rc=$?"
 E="python tools/kprof.py exact --queries 1000 --reps 1"
 $E > gpurun_out/kp_exact.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"k_exact" -c 1 -o gpurun_out/prof_exact $E \

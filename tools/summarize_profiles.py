@@ -66,9 +66,11 @@ print("\n".join(lines[:16]))
 
 traffic = {}
 summ = [f"# {rnd}: key metrics from `ncu --set full --clock-control none` (tools/profile_round.sh)", ""]
-for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one k_qt launch = 1e8 pairs)"),
-                  ("prof_knn.ncu-rep", "kprof knn --queries 1000 (the bench batch: one launch of each kernel per step)"),
+for rep, what in [("prof_knn.ncu-rep", "kprof knn --queries 1000 (the bench batch: one ft_knn call; the fused prefilter "
+                                     "is k_qt on the 1/32 sample, k_row_threshold, k_qt threshold scan, k_select_fast "
+                                     "on the lists, and the (idle) fallback k_qt / k_select_fast)"),
                   ("prof_ftd.ncu-rep", "kprof ft --queries 64 (exhaustive Flowtree over 100k docs: k_ftd + list-mode k_flowtree)"),
+                  ("prof_img.ncu-rep", "kprof ft --config image --queries 16 (exhaustive Flowtree over 60k image docs: k_flowtree)"),
                   ("prof_exact.ncu-rep", "kprof exact --queries 1000 (QT 424 -> FT 9 -> exact W1, transportation simplex)")]:
     p = os.path.join(OUT, rep)
     if not os.path.exists(p):
@@ -80,7 +82,9 @@ for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one
         for m, (v, u) in ms.items():
             summ.append(f"  {m} = {v} {u}")
         # the Flowtree stage is k_ftd plus the list-mode k_flowtree: their traffic is summed
-        key = {("k_qt", "prof_qt.ncu-rep"): "quadtree", ("k_dist_tc", "prof_knn.ncu-rep"): "dist_table",
+        # the quadtree stage = every prefilter kernel of the call; the Flowtree stage = k_ftd + k_flowtree
+        key = {("k_qt", "prof_knn.ncu-rep"): "quadtree", ("k_row_threshold", "prof_knn.ncu-rep"): "quadtree",
+               ("k_dist_i8", "prof_knn.ncu-rep"): "dist_table",
                ("k_ftd", "prof_knn.ncu-rep"): "flowtree", ("k_flowtree", "prof_knn.ncu-rep"): "flowtree"}.get(
             (short.split("<")[0], rep))
         if key:
@@ -93,8 +97,9 @@ for rep, what in [("prof_qt.ncu-rep", "kprof qt --queries 1000 (bench batch, one
         summ.append("")
 open(os.path.join(PROF, f"{rnd}_ncu_summary.txt"), "w").write("\n".join(summ) + "\n")
 if traffic:
-    traffic["source"] = (f"profiles/{rnd}_ncu_summary.txt: dram read+write of one ncu --set full launch (k_qt: the "
-                         "1000-query bench batch; k_dist_tc / k_ftd + k_flowtree: kprof knn on the same 1000-query "
-                         "batch, one launch each, as in the bench)")
+    traffic["source"] = (f"profiles/{rnd}_ncu_summary.txt: dram read+write of one ncu --set full capture of "
+                         "kprof knn on the 1000-query bench batch (one ft_knn call, as one bench step): quadtree = "
+                         "the k_qt launches + k_row_threshold of the fused prefilter; dist_table = k_dist_i8; "
+                         "flowtree = k_ftd + list-mode k_flowtree")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     print(traffic)
