@@ -78,3 +78,41 @@ __device__ __forceinline__ double fti_warp_sum_f64(double x) {
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
 }
+
+// Block-wide counting sort by a small key: every thread of the block passes key ∈ [0, 256] (256 =
+// "invalid, last"); returns the index of the thread whose key is the threadIdx.x-th smallest (the
+// order among equal keys is arbitrary).  hist: 260 ints of smem; perm: blockDim.x u16 of smem.
+// Three barriers and one warp scan instead of a bitonic network (36 barrier stages for 256 keys).
+__device__ __forceinline__ int fti_counting_rank(uint32_t key, int* hist, uint16_t* perm) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < 260; i += nt) hist[i] = 0;
+    __syncthreads();
+    const int r = atomicAdd(&hist[key], 1);
+    __syncthreads();
+    if (tid < 32) {   // exclusive scan of hist[0..256]: 9 buckets per lane
+        int v[9], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 9; k++) {
+            const int idx = tid * 9 + k;
+            v[k] = idx < 257 ? hist[idx] : 0;
+            sum += v[k];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        int b = incl - sum;
+#pragma unroll
+        for (int k = 0; k < 9; k++) {
+            const int idx = tid * 9 + k;
+            if (idx < 257) hist[idx] = b;
+            b += v[k];
+        }
+    }
+    __syncthreads();
+    perm[hist[key] + r] = (uint16_t)tid;
+    __syncthreads();
+    return perm[tid];
+}

@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     // uniform weights on both sides (every mass 1): the lean merge
     const bool uni = a.unit_w && U == sq;
     unsigned ubytes = 0;
-    __shared__ unsigned long long skey[DW * 32];
+    __shared__ int shist[260];
+    __shared__ uint16_t sperm[DW * 32];
     // table row offset of vocab id x (compact table: its candidate-vocabulary rank)
     auto row_off = [&](uint32_t x) -> uint32_t {
         uint32_t row = x;
@@ -141,19 +142,18 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
     for (int64_t cbase = (int64_t)blockIdx.x * DW * 32; cbase < a.n_docs; cbase += stride) {
         // the CTA's DW*32 positions sorted by doc support size, so the lanes of a warp run merges
         // of similar length (the warp steps until its longest pair is done)
+        // (a counting sort on the size: ≤ 254, 256 = past the end)
+        int tpos;
         {
             const int64_t p = cbase + threadIdx.x;
-            uint32_t sz = 0xFFFFFFFFu;
+            uint32_t key = 256u;
             if (p < a.n_docs) {
                 const int64_t doc = a.docs ? a.docs[(int64_t)q * a.docs_ld + p] : p;
-                sz = (doc >= 0 && doc < a.n) ? a.doc_off[doc + 1] - a.doc_off[doc] : 0u;
+                key = (doc >= 0 && doc < a.n) ? a.doc_off[doc + 1] - a.doc_off[doc] : 0u;
             }
-            __syncthreads();   // the previous chunk's keys are consumed
-            skey[threadIdx.x] = ((unsigned long long)sz << 32) | (uint32_t)threadIdx.x;
-            __syncthreads();
-            fti_bitonic_sort_u64(skey, DW * 32);
+            tpos = fti_counting_rank(key, shist, sperm);
         }
-        const int64_t dp = cbase + (int64_t)(uint32_t)skey[threadIdx.x];
+        const int64_t dp = cbase + tpos;
         bool active = false;
         int s = 0;
         uint32_t i0 = 0, W = 0;
@@ -332,6 +332,8 @@ __global__ void __launch_bounds__(DW * 32, FTD_MINB) k_ftd(DArgs a) {
                     if (EXPORT) { xc = ad ? xn : xc; xn = ad ? x2 : xn; }
                     // raw records loaded three advances before use (x3..x5: items i+3..i+5): the
                     // record load's latency had been the merge's largest stall
+                    // (a predicated inline-PTX load straight into x5's register, to avoid the select
+                    // on the fresh load: 2.89 -> 3.10 ms exhaustive, not kept)
                     if (ad) {
                         x2 = x3 & FTI_VOCAB_MASK;
                         x3 = x4;
