@@ -1,4 +1,7 @@
 set -u
 mkdir -p gpurun_out
-python tools/chunk_sweep.py reviews 0 256 128 64 32 16 > gpurun_out/chunk_reviews.log 2>&1
-python tools/chunk_sweep.py stress 0 128 64 32 16 > gpurun_out/chunk_stress.log 2>&1
+I="python tools/kprof.py ft --config image --queries 16 --reps 1"
+$I > gpurun_out/kp_img.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"k_ftg" -c 1 -o gpurun_out/prof_ftg $I \
+  > gpurun_out/ncu_ftg.log 2>&1
+echo "rc=$?" >> gpurun_out/ncu_ftg.log
