@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(256) k_row_threshold(const double* __restrict_
                                                        double* __restrict__ thr) {
     __shared__ unsigned hist[2048];
     __shared__ uint32_t s_pre, s_need;
+    __shared__ int s_tmp[32];
     const int row = blockIdx.x;
     const double* v = vals + (int64_t)row * ld;
     auto key_of = [](double x) -> uint32_t {
@@ -508,14 +509,23 @@ __global__ void __launch_bounds__(256) k_row_threshold(const double* __restrict_
             if ((k & pmask) == pre) atomicAdd(&hist[(k >> shift[p]) & dm], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t need = s_need, cum = 0u, b = 0u;
-            for (; b < dm; b++) {
-                if (cum + hist[b] > need) break;
-                cum += hist[b];
+        {
+            // the digit holding the need-th key: each thread sums a run of bins, a block scan places
+            // the runs, and the one thread whose run holds it walks its bins (a single thread
+            // walking all 2048 bins had made this kernel latency-bound: 0.19 ms per 1,000 rows)
+            const int nb = 1 << width[p], per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
+            const int b0 = (int)threadIdx.x * per;
+            uint32_t run = 0u;
+            for (int j = 0; j < per && b0 + j < nb; j++) run += hist[b0 + j];
+            const uint32_t need = s_need;
+            const uint32_t before = (uint32_t)fti_block_exclusive_sum((int)run, s_tmp, nullptr);
+            if (run > 0u && before <= need && need < before + run) {
+                uint32_t cum = before;
+                int b = b0;
+                while (cum + hist[b] <= need) { cum += hist[b]; b++; }
+                s_need = need - cum;
+                s_pre = pre | ((uint32_t)b << shift[p]);
             }
-            s_need = need - cum;
-            s_pre = pre | (b << shift[p]);
         }
         pmask |= dm << shift[p];
         __syncthreads();

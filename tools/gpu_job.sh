@@ -1,7 +1,5 @@
 set -u
 mkdir -p gpurun_out
-I="python tools/kprof.py ft --config image --queries 16 --reps 1"
-$I > gpurun_out/kp_img.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_ftg" -c 1 -o gpurun_out/prof_ftg $I \
-  > gpurun_out/ncu_ftg.log 2>&1
-echo "rc=$?" >> gpurun_out/ncu_ftg.log
+python -m pytest tests/test_parity_gpu.py -x -q -k "knn or prefilter or select or threshold or full_size_sampled or lists" > gpurun_out/pytest_small.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_small.log
+python tools/chunk_sweep.py reviews 0 > gpurun_out/stages.log 2>&1
+python tools/chunk_sweep.py stress 0 >> gpurun_out/stages.log 2>&1
