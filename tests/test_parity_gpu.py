@@ -5,6 +5,7 @@ values within 1e-5 relative (oracle 0 ⇒ GPU exactly 0); final top-k ids exact 
 (oracle values within 2·tol of a rank boundary may permute among themselves).
 """
 import concurrent.futures as cf
+import os
 
 import numpy as np
 import pytest
@@ -866,3 +867,21 @@ def test_topk_threshold_tie_blocks(ft):
         o = np.lexsort((np.arange(L), vals[r]))[:k]
         assert np.array_equal(oi[r], o), r
         assert np.array_equal(ov[r], vals[r][o])
+
+
+def test_bounds_checked_build_runs_clean(ft):
+    """compute-sanitizer is closed on this GPU pool, so the stand-in: the library rebuilt with
+    FTI_CHECKED (device-side asserts on every table gather and store, the per-lane queues, the row
+    maps and the staged arrays) runs the sanitizer workload (tools/sanitize_run.py: tiny, a 2,000-doc
+    reviews subset through the tcgen05 distance table, k_ftd and its warp-kernel hand-over, the
+    selection kernels and the exact-W1 simplex, and an image subset) in a fresh process; a failed
+    device assert aborts that process."""
+    import subprocess
+    import sys
+    from paper_1910_04126_b200 import build
+    lib = build.build(checked=True)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FT_LIB=lib)
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0 and "sanitize workload ok" in p.stdout, (p.returncode, p.stdout[-2000:], p.stderr[-4000:])

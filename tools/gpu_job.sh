@@ -1,5 +1,4 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_parity_gpu.py -x -q -k "knn or prefilter or select or threshold or full_size_sampled or lists" > gpurun_out/pytest_small.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_small.log
-python tools/chunk_sweep.py reviews 0 > gpurun_out/stages.log 2>&1
-python tools/chunk_sweep.py stress 0 >> gpurun_out/stages.log 2>&1
+which compute-sanitizer > gpurun_out/san.log 2>&1; ls /usr/local/cuda/bin/compute-sanitizer >> gpurun_out/san.log 2>&1
+timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_run.py >> gpurun_out/san.log 2>&1; echo "memcheck rc $?" >> gpurun_out/san.log
