@@ -280,6 +280,7 @@ struct QtArgs {
     int64_t out_ld;
     int d_star, l_root;
     double pow2;                // 2^{ℓ_root − D*} when it is a normal double (0: use scalbn)
+    float pow2f;                // the same as a normal float (0: the threshold screen is off)
     int wide;                   // D* > 31: the U·A and W·B products can overflow 64 bits
     uint32_t* err;
     // threshold mode (the fused prefilter): instead of writing out, append (value, doc) to query q's
@@ -296,8 +297,27 @@ struct QtArgs {
 
 // lane q: QT(q, doc) = (U A + W B_q − 2 acc) · 2^{ℓ_root − D*} / (W U), exact u64 numerator, two
 // correctly rounded FP64 operations (NaN for an invalid query or an overflowing numerator)
+// Threshold mode: thr_l is the lane's threshold, thr_hi an FP32 bound above it — a value whose FP32
+// estimate exceeds thr_hi is certainly above thr_l (the estimate is within 2^-21 relative of the
+// exact quotient), so most docs skip the FP64 division; the rest take the exact path.
+struct QtThr {
+    double t;
+    float hi;
+};
+__device__ __forceinline__ QtThr qt_thr(const QtArgs& a, int nqc) {
+    const int lane = threadIdx.x & 31;
+    QtThr r{0.0, 0.f};
+    if (a.thr && lane < nqc) {
+        r.t = a.thr[(int64_t)(blockIdx.y * QT_QC + lane) * a.thr_ld];
+        r.hi = a.pow2f != 0.f ? __fmul_ru(__double2float_ru(r.t), 1.0f + 0x1p-18f) : __int_as_float(0x7f800000);
+        if (r.t != r.t) r.hi = -1.f;   // NaN threshold: nothing passes (and the exact path agrees)
+    }
+    return r;
+}
+
 __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int64_t dp, int64_t doc,
-                                         unsigned long long acc, uint32_t W32, unsigned long long A) {
+                                         unsigned long long acc, uint32_t W32, unsigned long long A,
+                                         const QtThr& th) {
     const int lane = threadIdx.x & 31;
     if (lane >= nqc) return;
     const int q = blockIdx.y * QT_QC + lane;
@@ -314,6 +334,12 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
         bad = true;
         atomicOr(a.err, FTI_ERR_OVERFLOW);
     }
+    if (a.thr && !bad) {
+        // FP32 screen: (float)num, (float)(U·W), the power of two and the reciprocal each round
+        // by ≤ 1 ulp (≤ 2^-21 relative in all), far inside the 2^-18 margin of th.hi
+        const float est = __fmul_rn(__fmul_rn(__ull2float_rn(num), a.pow2f), __frcp_rn(__ull2float_rn(Uq * W)));
+        if (est > th.hi) return;
+    }
     if (bad) {
         val = __longlong_as_double(0x7ff8000000000000ll);
     } else {
@@ -322,7 +348,7 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
         val = __ddiv_rn(scaled, (double)(Uq * W));
     }
     if (a.thr) {
-        if (!bad && val <= a.thr[(int64_t)q * a.thr_ld]) {
+        if (!bad && val <= th.t) {
             const uint32_t pos = atomicAdd(&a.ccnt[q], 1u);
             if ((int64_t)pos < a.ccap) {
                 a.cval[(int64_t)q * a.ccap + pos] = val;
@@ -345,6 +371,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
                                               uint4* __restrict__ hq, const ChunkHdr& sh, int nqc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const QtThr th = qt_thr(a, nqc);
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
@@ -404,7 +431,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             }
             __syncwarp();
         }
-        qt_store(a, sh, nqc, dp, doc, acc, W32, A);
+        qt_store(a, sh, nqc, dp, doc, acc, W32, A, th);
     }
 }
 
@@ -416,6 +443,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                                         const uint16_t* __restrict__ idxs, const ChunkHdr& sh, int nqc) {
     const ChunkGeom& g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const QtThr th = qt_thr(a, nqc);
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
@@ -469,7 +497,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 visit(e2, m2);
             }
         }
-        qt_store(a, sh, nqc, dp, doc, acc, W32, A);
+        qt_store(a, sh, nqc, dp, doc, acc, W32, A, th);
     }
 }
 
@@ -601,6 +629,7 @@ cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* 
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
     a.pow2 = std::abs(a.l_root - a.d_star) <= 960 ? std::ldexp(1.0, a.l_root - a.d_star) : 0.0;
+    a.pow2f = std::abs(a.l_root - a.d_star) <= 100 ? std::ldexp(1.0f, a.l_root - a.d_star) : 0.0f;
     a.wide = a.d_star > 31 ? 1 : 0;
     a.err = ds->err_dev;
     const int64_t target = (int64_t)148 * P.ctas_per_sm * waves;

@@ -162,3 +162,72 @@ def test_two_rank_gloo_sharded_knn(tmp_path):
     for q, ids, vals in flat:
         ref_ids, ref_vals = T.knn(wl.doc_off, wl.ids, wl.w, *wl.query(q), wl.k, 30)
         assert ids == ref_ids.tolist() and vals == ref_vals.tolist()
+
+
+class _HostCollectives:
+    """torch.distributed over gloo with the library's CUDA tensors staged through host memory (the
+    protocol's collectives; on a multi-GPU node they run on NCCL device buffers instead)."""
+
+    def __init__(self, dist):
+        self.d = dist
+        self.ReduceOp = dist.ReduceOp
+
+    def is_initialized(self):
+        return self.d.is_initialized()
+
+    def get_world_size(self):
+        return self.d.get_world_size()
+
+    def all_gather(self, outs, t):
+        host = [o.cpu() for o in outs]
+        self.d.all_gather(host, t.cpu())
+        for o, h in zip(outs, host):
+            o.copy_(h)
+
+    def all_reduce(self, t, op):
+        h = t.cpu()
+        self.d.all_reduce(h, op=op)
+        t.copy_(h)
+
+
+def _lib_doc_worker(rank, world, port, result_path, name, n_docs, nq, m):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1910_04126_b200 import flowtree as ft, parallel, workloads
+    wl = workloads.make(name, n_docs=n_docs, n_queries=nq) if name != "tiny" else workloads.make("tiny")
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    d_off, d_ids, d_w, base = parallel.shard_docs(wl.doc_off, wl.ids, wl.w, rank, world)
+    ds = ft.Dataset(ix, d_off, d_ids, d_w)
+    ids, vals = parallel.knn_doc_sharded(parallel.LibShard(ft, ds, base), wl.q_off, wl.q_ids, wl.q_w, wl.k, m,
+                                         _HostCollectives(dist))
+    if rank == 0:
+        np.save(result_path, np.array([ids.cpu().numpy(), vals.cpu().numpy()], dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n_docs,nq,m", [("reviews", 3000, 6, 200), ("tiny", None, None, 30)])
+def test_two_process_library_doc_sharded_knn(tmp_path, name, n_docs, nq, m):
+    """Doc sharding with the LIBRARY on each rank — Quadtree + ft_topk local top-m,
+    all-gather, merge, the owned candidates' Flowtree through the distance table (d = 300), MIN
+    all-reduce, top-k — in two processes (world size 2, gloo; one GPU shared, the ranks' kernels
+    never wait on one another): bit-identical to a single ft_knn over the whole collection."""
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path / "res_lib.npy")
+    mp.spawn(_lib_doc_worker, args=(2, _free_port(), out, name, n_docs, nq, m), nprocs=2, join=True)
+    ids, vals = np.load(out, allow_pickle=True)
+    from paper_1910_04126_b200 import flowtree as ft, workloads
+    wl = workloads.make(name, n_docs=n_docs, n_queries=nq) if name != "tiny" else workloads.make("tiny")
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    ref_ids, ref_vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, wl.k, m)
+    assert np.array_equal(ids, ref_ids) and np.array_equal(vals, ref_vals)
