@@ -1,3 +1,6 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_multiproc.py tests/test_parity_gpu.py -x -q -m gpu -k "library_doc_sharded or bounds_checked or two_shard" > gpurun_out/pytest_mp.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_mp.log
+python -m pytest tests -x -q -m gpu --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+bash tools/profile_round.sh > gpurun_out/profile_round.log 2>&1
