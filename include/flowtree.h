@@ -193,6 +193,7 @@ uint64_t ft_launch_count(void);
  *   FT_OPT_FTD_CARVEOUT    1..100: k_ftd shared-memory carveout percent (0: sized for 3 CTAs/SM).
  *   FT_OPT_PREFILTER_UNFUSED 1: ft_knn's prefilter writes every Quadtree value and then selects
  *                          (the fused sample-threshold scan is the default when n ≥ 32·m).
+ *   FT_OPT_QT_PAIR_OFF     1: the Quadtree scan serves 32 queries per record pass (no chunk pairs).
  *   FT_OPT_DEBUG           bit mask of diagnostics printed to stderr: 1 distance-table role
  *                          clocks, 2 exact-W1 pivots, 4 selection paths, 8 scratch growth; and
  *                          16: ft_flowtree_flow fails (FT_ESTATE) unless the lane-per-pair kernel
@@ -209,7 +210,8 @@ typedef enum {
     FT_OPT_FTD_CARVEOUT = 8,
     FT_OPT_DEBUG = 9,
     FT_OPT_PREFILTER_UNFUSED = 10,
-    FT_NUM_OPTIONS = 11
+    FT_OPT_QT_PAIR_OFF = 11,
+    FT_NUM_OPTIONS = 12
 } ft_option;
 ft_status ft_set_option(int32_t option, int64_t value);
 ft_status ft_get_option(int32_t option, int64_t* value);

@@ -183,6 +183,7 @@ struct ft_dataset {
     DevBuf s_map, s_rows, s_rowcnt, s_table, s_flow, s_flowcnt, s_vlist, s_chunk, s_rowbase, s_bsplit, s_ny, s_tiles, s_qinfo, s_wdesc, s_wrow, s_sel, s_chunkd, s_fblist, s_fbcnt, s_topk;
     // fused prefilter (fti_launch_prefilter): sample doc ids, sample values, thresholds, lists
     DevBuf s_pf_samp, s_pf_sval, s_pf_tval, s_pf_cnt, s_pf_cval, s_pf_cid, s_pf_bad, s_pf_flag;
+    DevBuf s_chunkd2;   // Quadtree chunk-pair dense structures (ft_qt.cu)
     int64_t pf_ns = -1;
 };
 

@@ -197,6 +197,11 @@ struct DenseGeom {
     int mw;          // bitmap words = ceil(M / 32)
     int cap;         // max union size (0: dense path disabled)
     size_t stride;   // bytes per chunk: header | bits[mw] | rank[mw] | post[cap][32]
+    // chunk PAIRS (64 queries, lane l = queries l and 32 + l of the pair): the union of both
+    // chunks' nodes, and per union node a u16 per lane packing the two queries' masses as bytes
+    // (only when every mass < 256, e.g. unit weights); one record pass then serves 64 queries
+    int cap2;        // max union size of a pair (0: pair path disabled)
+    size_t stride2;  // bytes per pair: header | bits[mw] | rank[mw] | post2[cap2][32] u16
 };
 
 struct DenseHdr {
@@ -262,6 +267,72 @@ __global__ void __launch_bounds__(1024) k_qt_dense(const uint8_t* __restrict__ q
     if (threadIdx.x == 0) { hdr->flag = 1u; hdr->nU = (uint32_t)nU; }
 }
 
+// Dense structure of a chunk PAIR (queries 64c .. 64c + 63): flag 0 when the union exceeds cap2 or
+// a query node mass does not fit a byte (those pairs are scanned chunk by chunk).
+__global__ void __launch_bounds__(1024) k_qt_dense2(const uint8_t* __restrict__ qblock, QueryLayout L, int32_t nq,
+                                                    DenseGeom dg, uint8_t* __restrict__ dchunks) {
+    extern __shared__ uint32_t sd[];
+    uint32_t* bits = sd;              // mw
+    uint32_t* rank = sd + dg.mw;      // mw
+    __shared__ int tmp[32];
+    __shared__ int s_big;
+    const int c = blockIdx.x;
+    const int q0 = c * 2 * QT_QC;
+    const int nqc = min(2 * QT_QC, nq - q0);
+    uint8_t* out = dchunks + (size_t)c * dg.stride2;
+    DenseHdr* hdr = (DenseHdr*)out;
+    for (int i = threadIdx.x; i < dg.mw; i += blockDim.x) bits[i] = 0u;
+    if (threadIdx.x == 0) s_big = 0;
+    __syncthreads();
+    const int slots = L.nh_cap;
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        atomicOr(&bits[e.x >> 5], 1u << (e.x & 31u));
+        if ((e.y & 0xFFFFu) > 255u) s_big = 1;
+    }
+    __syncthreads();
+    int run = 0;
+    for (int b0 = 0; b0 < dg.mw; b0 += blockDim.x) {
+        const int w = b0 + threadIdx.x;
+        const int v = w < dg.mw ? __popc(bits[w]) : 0;
+        int tot;
+        const int r = run + fti_block_exclusive_sum(v, tmp, &tot);
+        if (w < dg.mw) rank[w] = (uint32_t)r;
+        run += tot;
+    }
+    __syncthreads();
+    const int nU = run;
+    if (nU > dg.cap2 || s_big) {
+        if (threadIdx.x == 0) { hdr->flag = 0u; hdr->nU = (uint32_t)nU; }
+        return;
+    }
+    uint32_t* gbits = (uint32_t*)(out + sizeof(DenseHdr));
+    uint32_t* grank = gbits + dg.mw;
+    uint32_t* gpost = grank + dg.mw;                       // [nU][32] u16, as u32 pairs of lanes
+    for (int i = threadIdx.x; i < dg.mw; i += blockDim.x) { gbits[i] = bits[i]; grank[i] = rank[i]; }
+    for (int i = threadIdx.x; i < nU * QT_QC / 2; i += blockDim.x) gpost[i] = 0u;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nqc * slots; t += blockDim.x) {
+        const int ql = t / slots, s = t - ql * slots;
+        const uint8_t* slot = qblock + (size_t)(q0 + ql) * L.stride;
+        const QHeader* qh = (const QHeader*)slot;
+        if (qh->err || s > (int)qh->nh_mask) continue;
+        const uint2 e = ((const uint2*)(slot + L.off_nh))[s];
+        if (e.x == FTI_EMPTY) continue;
+        const uint32_t bw = bits[e.x >> 5], bpos = e.x & 31u;
+        const uint32_t id = rank[e.x >> 5] + __popc(bw & ((1u << bpos) - 1u));
+        const uint32_t ln = (uint32_t)ql & 31u, hi = (uint32_t)ql >> 5;   // lane, which chunk of the pair
+        const uint32_t v = (e.y & 0xFFu) << (8u * hi + 16u * (ln & 1u));
+        atomicOr(&gpost[(id * QT_QC + ln) >> 1], v);
+    }
+    if (threadIdx.x == 0) { hdr->flag = 1u; hdr->nU = (uint32_t)nU; }
+}
+
 struct QtArgs {
     const uint32_t* qt_off;
     const uint2* qt;
@@ -293,6 +364,10 @@ struct QtArgs {
     int64_t ccap;
     // fallback mode: only the chunks holding a flagged query run, and only flagged rows are written
     const uint32_t* qflag;
+    // pair mode: each CTA row (blockIdx.y) covers chunks 2y and 2y + 1
+    int pair;
+    int nchunks;
+    const uint8_t* dchunks2;
 };
 
 // lane q: QT(q, doc) = (U A + W B_q − 2 acc) · 2^{ℓ_root − D*} / (W U), exact u64 numerator, two
@@ -304,23 +379,23 @@ struct QtThr {
     double t;
     float hi;
 };
-__device__ __forceinline__ QtThr qt_thr(const QtArgs& a, int nqc) {
+__device__ __forceinline__ QtThr qt_thr(const QtArgs& a, int nqc, int cy) {
     const int lane = threadIdx.x & 31;
     QtThr r{0.0, 0.f};
     if (a.thr && lane < nqc) {
-        r.t = a.thr[(int64_t)(blockIdx.y * QT_QC + lane) * a.thr_ld];
+        r.t = a.thr[(int64_t)(cy * QT_QC + lane) * a.thr_ld];
         r.hi = a.pow2f != 0.f ? __fmul_ru(__double2float_ru(r.t), 1.0f + 0x1p-18f) : __int_as_float(0x7f800000);
         if (r.t != r.t) r.hi = -1.f;   // NaN threshold: nothing passes (and the exact path agrees)
     }
     return r;
 }
 
-__device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int64_t dp, int64_t doc,
-                                         unsigned long long acc, uint32_t W32, unsigned long long A,
+__device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, int nqc, int cy, int64_t dp,
+                                         int64_t doc, unsigned long long acc, uint32_t W32, unsigned long long A,
                                          const QtThr& th) {
     const int lane = threadIdx.x & 31;
     if (lane >= nqc) return;
-    const int q = blockIdx.y * QT_QC + lane;
+    const int q = cy * QT_QC + lane;
     const unsigned long long Uq = sh.U[lane], Bq = sh.B[lane], W = W32;
     double val;
     bool bad = !sh.ok[lane];
@@ -369,9 +444,9 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
 template <bool WIDE>
 __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* __restrict__ bits,
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
-                                              uint4* __restrict__ hq, const ChunkHdr& sh, int nqc) {
+                                              uint4* __restrict__ hq, const ChunkHdr& sh, int nqc, int cy) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const QtThr th = qt_thr(a, nqc);
+    const QtThr th = qt_thr(a, nqc, cy);
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
@@ -380,7 +455,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
         const int64_t doc = a.docs ? a.docs[dp] : dp;
         if (doc < 0 || doc >= a.n) {
             if (lane < nqc && !a.thr)
-                a.out[(int64_t)(blockIdx.y * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+                a.out[(int64_t)(cy * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
             if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
             continue;
         }
@@ -431,7 +506,84 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
             }
             __syncwarp();
         }
-        qt_store(a, sh, nqc, dp, doc, acc, W32, A, th);
+        qt_store(a, sh, nqc, cy, dp, doc, acc, W32, A, th);
+    }
+}
+
+// Pair scan (dense pair structure): lane l scores queries l of chunk cy and l of chunk cy + 1; each
+// hit reads one u16 per lane holding both queries' masses, so a record pass, its membership tests
+// and the hit compaction serve 64 queries.
+template <bool WIDE>
+__device__ __forceinline__ void qt_scan_dense2(const QtArgs& a, const uint32_t* __restrict__ bits,
+                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
+                                               uint4* __restrict__ hq, const ChunkHdr& sa, const ChunkHdr& sb,
+                                               int cy) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int na = (int)sa.nq, nb = (int)sb.nq;
+    const QtThr tha = qt_thr(a, na, cy), thb = qt_thr(a, nb, cy + 1);
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t Ua = sa.U[lane], Ub = sb.U[lane];
+    const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
+    const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
+    for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
+        const int64_t doc = a.docs ? a.docs[dp] : dp;
+        if (doc < 0 || doc >= a.n) {
+            if (!a.thr) {
+                if (lane < na) a.out[(int64_t)(cy * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+                if (lane < nb)
+                    a.out[(int64_t)((cy + 1) * QT_QC + lane) * a.out_ld + dp] = __longlong_as_double(0x7ff8000000000000ll);
+            }
+            if (lane == 0) atomicOr(a.err, FTI_ERR_RANGE);
+            continue;
+        }
+        const uint32_t r0 = a.qt_off[doc], r1 = a.qt_off[doc + 1];
+        const uint32_t W32 = a.W[doc];
+        const unsigned long long A = a.A[doc];
+        unsigned long long acca = 0, accb = 0;
+        auto term = [&](uint32_t p, uint32_t mmu, uint32_t f_) {
+            // masses < 256 here: U·m_μ and W·m_ν < 2^32, 64-bit accumulation as in the 32-query scan
+            const uint32_t wa = W32 * (p & 0xFFu), wb = W32 * (p >> 8);
+            const uint32_t ua = Ua * mmu, ub = Ub * mmu;
+            if (WIDE) {
+                acca += (unsigned long long)(ua < wa ? ua : wa) << f_;
+                accb += (unsigned long long)(ub < wb ? ub : wb) << f_;
+            } else {
+                acca += (unsigned long long)(ua < wa ? ua : wa) * f_;
+                accb += (unsigned long long)(ub < wb ? ub : wb) * f_;
+            }
+        };
+        for (uint32_t rb = r0; rb < r1; rb += 32) {
+            const uint32_t r = rb + lane;
+            int id = -1;
+            uint32_t y = 0;
+            if (r < r1) {
+                const uint2 rec = a.qt[r];
+                y = rec.y;
+                const uint32_t bw = bits[rec.x >> 5], bpos = rec.x & 31u;
+                if ((bw >> bpos) & 1u) id = (int)(rank[rec.x >> 5] + __popc(bw & ((1u << bpos) - 1u)));
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, id >= 0);
+            const int nh = __popc(hm);
+            if (id >= 0)
+                hq[__popc(hm & lt)] = make_uint4((uint32_t)id * QT_QC, y & 0xFFFFu,
+                                                 WIDE ? (uint32_t)(a.d_star - (int)(y >> 16))
+                                                      : 1u << (a.d_star - (int)(y >> 16)),
+                                                 0u);
+            if (nh & 1) {
+                if (lane == 0) hq[nh] = make_uint4(0u, 0u, 0u, 0u);      // pad: mass 0 contributes 0
+            }
+            __syncwarp();
+            for (int h = 0; h < nh; h += 2) {
+                const uint4 e1 = hq[h], e2 = hq[h + 1];
+                const uint32_t p1 = post[e1.x + lane];
+                const uint32_t p2 = post[e2.x + lane];
+                term(p1, e1.y, e1.z);
+                term(p2, e2.y, e2.z);
+            }
+            __syncwarp();
+        }
+        qt_store(a, sa, na, cy, dp, doc, acca, W32, A, tha);
+        qt_store(a, sb, nb, cy + 1, dp, doc, accb, W32, A, thb);
     }
 }
 
@@ -440,14 +592,14 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
 template <bool SMEM>
 __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restrict__ keys,
                                         const uint2* __restrict__ ent, const uint32_t* __restrict__ post,
-                                        const uint16_t* __restrict__ idxs, const ChunkHdr& sh, int nqc) {
+                                        const uint16_t* __restrict__ idxs, const ChunkHdr& sh, int nqc, int cy) {
     const ChunkGeom& g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const QtThr th = qt_thr(a, nqc);
+    const QtThr th = qt_thr(a, nqc, cy);
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
-    const int q = blockIdx.y * QT_QC + lane;
+    const int q = cy * QT_QC + lane;
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
     const int64_t d1 = min(a.n_docs, d0 + a.docs_per_cta);
     for (int64_t dp = d0 + warp; dp < d1; dp += QT_WARPS) {
@@ -497,29 +649,21 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                 visit(e2, m2);
             }
         }
-        qt_store(a, sh, nqc, dp, doc, acc, W32, A, th);
+        qt_store(a, sh, nqc, cy, dp, doc, acc, W32, A, th);
     }
 }
 
-__global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
+// the scan of chunk cy by this CTA (dense or hash structure)
+__device__ __forceinline__ void qt_chunk(const QtArgs& a, int cy, ChunkHdr& sh, DenseHdr& dh) {
     extern __shared__ uint32_t sm[];
-    __shared__ ChunkHdr sh;
     const ChunkGeom& g = a.g;
     uint32_t* keys = sm;                                  // cap
     uint2* ent_s = (uint2*)(keys + g.cap);                // ucap_s {query mask, posting offset}
     uint32_t* post_s = (uint32_t*)(ent_s + g.ucap_s);     // pcap_s
     uint16_t* idxs = (uint16_t*)(post_s + g.pcap_s);      // cap
-    if (a.qflag) {   // fallback mode: chunks without a flagged query have nothing to do
-        int f = 0;
-        if (threadIdx.x < QT_QC) {
-            const int q = blockIdx.y * QT_QC + threadIdx.x;
-            f = q < a.nq && a.qflag[q] != 0u;
-        }
-        if (!__syncthreads_or(f)) return;
-    }
-    const uint8_t* src = a.chunks + (size_t)blockIdx.y * g.stride;
-    __shared__ DenseHdr dh;
-    const uint8_t* dsrc = a.dchunks ? a.dchunks + (size_t)blockIdx.y * a.dg.stride : nullptr;
+    const uint8_t* src = a.chunks + (size_t)cy * g.stride;
+    const uint8_t* dsrc = a.dchunks ? a.dchunks + (size_t)cy * a.dg.stride : nullptr;
+    __syncthreads();   // the previous chunk's structures are consumed
     if (threadIdx.x == 0) {
         sh = *(const ChunkHdr*)src;
         dh = dsrc ? *(const DenseHdr*)dsrc : DenseHdr{0u, 0u, 0u, 0u};
@@ -535,9 +679,9 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
         uint4* hq = (uint4*)(sm + ((2 * a.dg.mw + a.dg.cap * QT_QC / 2 + 3) & ~3));   // per-warp hit queues
         __syncthreads();
         if (a.d_star > 31)
-            qt_scan_dense<true>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
+            qt_scan_dense<true>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq, cy);
         else
-            qt_scan_dense<false>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq);
+            qt_scan_dense<false>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, (int)sh.nq, cy);
         return;
     }
     const int nU = (int)sh.nU, nP = min((int)sh.nP, g.pmax), nqc = (int)sh.nq;
@@ -558,9 +702,52 @@ __global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
     }
     __syncthreads();
     if (nU <= g.ucap_s && nP <= g.pcap_s)
-        qt_scan<true>(a, keys, ent_s, post_s, idxs, sh, nqc);
+        qt_scan<true>(a, keys, ent_s, post_s, idxs, sh, nqc, cy);
     else
-        qt_scan<false>(a, keys, ent, post, idxs, sh, nqc);
+        qt_scan<false>(a, keys, ent, post, idxs, sh, nqc, cy);
+}
+
+// grid.y = chunks (or chunk pairs in pair mode), grid.x = doc ranges
+__global__ void __launch_bounds__(QT_WARPS * 32) k_qt(QtArgs a) {
+    extern __shared__ uint32_t sm[];
+    __shared__ ChunkHdr sh, sh2;
+    __shared__ DenseHdr dh;
+    const int per = a.pair ? 2 : 1;
+    const int cy0 = (int)blockIdx.y * per;
+    const int cy1 = min(a.nchunks, cy0 + per);
+    if (a.qflag) {   // fallback mode: chunks without a flagged query have nothing to do
+        int f = 0;
+        if (threadIdx.x < per * QT_QC) {
+            const int q = cy0 * QT_QC + threadIdx.x;
+            f = q < a.nq && a.qflag[q] != 0u;
+        }
+        if (!__syncthreads_or(f)) return;
+    }
+    if (a.pair && cy1 - cy0 == 2) {
+        const uint8_t* d2 = a.dchunks2 + (size_t)blockIdx.y * a.dg.stride2;
+        if (threadIdx.x == 0) {
+            dh = *(const DenseHdr*)d2;
+            sh = *(const ChunkHdr*)(a.chunks + (size_t)cy0 * a.g.stride);
+            sh2 = *(const ChunkHdr*)(a.chunks + (size_t)(cy0 + 1) * a.g.stride);
+        }
+        __syncthreads();
+        if (dh.flag) {
+            uint32_t* bits = sm;
+            uint32_t* rank = sm + a.dg.mw;
+            uint16_t* post = (uint16_t*)(rank + a.dg.mw);
+            const uint32_t* gb = (const uint32_t*)(d2 + sizeof(DenseHdr));
+            const int nwords = 2 * a.dg.mw + (int)dh.nU * QT_QC / 2;
+            for (int i = threadIdx.x; i < nwords; i += blockDim.x) sm[i] = gb[i];
+            uint4* hq = (uint4*)(sm + ((2 * a.dg.mw + a.dg.cap2 * QT_QC / 2 + 3) & ~3));
+            __syncthreads();
+            if (a.d_star > 31)
+                qt_scan_dense2<true>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, sh2, cy0);
+            else
+                qt_scan_dense2<false>(a, bits, rank, post, hq + (threadIdx.x >> 5) * 32, sh, sh2, cy0);
+            return;
+        }
+    }
+    for (int cy = cy0; cy < cy1; cy++) qt_chunk(a, cy, sh, dh);
 }
 
 }  // namespace
@@ -606,9 +793,26 @@ cudaError_t qt_prepare(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qb
         k_qt_dense<<<P.nchunks, 1024, smem_d, st>>>(d_qblock, L, nq, dg, ds->s_chunkd.as<uint8_t>());
         fti_count_launches(1);
     }
+    // chunk pairs (64 queries per record pass) when the dense path is on and there are ≥ 2 chunks
+    dg.cap2 = 0;
+    dg.stride2 = 0;
+    if (dg.cap > 0 && P.nchunks >= 2 && !fti_opt(FT_OPT_QT_PAIR_OFF)) {
+        const size_t avail = (size_t)212 * 1024 - (size_t)dg.mw * 8 - (size_t)QT_WARPS * 32 * 16;
+        dg.cap2 = (int)std::min<size_t>(2880, avail / (QT_QC * 2)) & ~31;
+        dg.stride2 = (sizeof(DenseHdr) + (size_t)dg.mw * 8 + (size_t)dg.cap2 * QT_QC * 2 + 15) / 16 * 16;
+        const int npairs = (P.nchunks + 1) / 2;
+        e = ds->s_chunkd2.reserve(dg.stride2 * (size_t)npairs);
+        if (e != cudaSuccess) return e;
+        const size_t smem_d = (size_t)dg.mw * 8;
+        e = cudaFuncSetAttribute(k_qt_dense2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        if (e != cudaSuccess) return e;
+        k_qt_dense2<<<npairs, 1024, smem_d, st>>>(d_qblock, L, nq, dg, ds->s_chunkd2.as<uint8_t>());
+        fti_count_launches(1);
+    }
+    const size_t hqb = (size_t)QT_WARPS * 32 * 16;
     P.smem = std::max<size_t>(4ull * P.g.cap + 8ull * P.g.ucap_s + 4ull * P.g.pcap_s + 2ull * P.g.cap,
-                              dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 16 + (size_t)QT_WARPS * 32 * 16
-                                         : 0);
+                              dg.cap > 0 ? (size_t)dg.mw * 8 + (size_t)dg.cap * QT_QC * 2 + 16 + hqb : 0);
+    if (dg.cap2 > 0) P.smem = std::max(P.smem, (size_t)dg.mw * 8 + (size_t)dg.cap2 * QT_QC * 2 + 16 + hqb);
     e = cudaFuncSetAttribute(k_qt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem);
     if (e != cudaSuccess) return e;
     P.ctas_per_sm = 0;
@@ -625,6 +829,9 @@ cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* 
     a.qt_off = ds->qt_off; a.qt = ds->qt; a.W = ds->W; a.A = ds->A;
     a.chunks = ds->s_chunk.as<uint8_t>(); a.g = P.g;
     a.dchunks = P.dg.cap > 0 ? ds->s_chunkd.as<uint8_t>() : nullptr; a.dg = P.dg;
+    a.pair = P.dg.cap2 > 0 ? 1 : 0;
+    a.nchunks = P.nchunks;
+    a.dchunks2 = a.pair ? ds->s_chunkd2.as<uint8_t>() : nullptr;
     a.nq = nq; a.docs = d_docs; a.n_docs = n_docs; a.n = ds->n;
     a.out = d_out; a.out_ld = out_ld;
     a.d_star = ds->ix->d_star; a.l_root = ds->ix->l_root;
@@ -633,10 +840,12 @@ cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* 
     a.wide = a.d_star > 31 ? 1 : 0;
     a.err = ds->err_dev;
     const int64_t target = (int64_t)148 * P.ctas_per_sm * waves;
-    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + P.nchunks - 1) / P.nchunks));
+    const int64_t rows_y = P.dg.cap2 > 0 ? (P.nchunks + 1) / 2 : P.nchunks;
+    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + rows_y - 1) / rows_y));
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
-    k_qt<<<dim3((unsigned)bx, (unsigned)P.nchunks), QT_WARPS * 32, P.smem, st>>>(a);
+    const int gy = a.pair ? (P.nchunks + 1) / 2 : P.nchunks;
+    k_qt<<<dim3((unsigned)bx, (unsigned)gy), QT_WARPS * 32, P.smem, st>>>(a);
     fti_count_launches(1);
     return cudaGetLastError();
 }

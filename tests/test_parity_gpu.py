@@ -485,6 +485,27 @@ def test_knn_tiny(ft, prefilter_m):
         assert_ft_close(vals[q], [ftv[i] for i in ids[q]])
 
 
+@pytest.mark.parametrize("name,n_docs,nq", [("reviews", 3000, 70), ("stress", 4000, 64), ("image", 800, 65),
+                                           ("text", 600, 33)])
+def test_quadtree_chunk_pairs_bit_identical(ft, opt, name, n_docs, nq):
+    """The Quadtree scan serves 64 queries per record pass (chunk pairs: a u16 per lane packing two
+    queries' node masses as bytes) when every query node mass fits a byte; otherwise, or for the odd
+    last chunk, chunk by chunk.  Values bit-identical with FT_OPT_QT_PAIR_OFF, and exact against the
+    oracle on sampled pairs (image: node masses ≥ 256 take the per-chunk path)."""
+    wl = get_workload(name, n_docs=n_docs, n_queries=nq)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    a = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    opt("FT_OPT_QT_PAIR_OFF")
+    b = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    assert np.array_equal(a, b)
+    rng = np.random.default_rng(9)
+    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, wl.nq, 60), rng.integers(0, wl.n, 60))]
+    pairs += [(wl.nq - 1, 0), (32, wl.n - 1), (63 if wl.nq > 63 else 0, 1)]
+    ref = _oracle_all(T, wl, "qt", pairs)
+    assert np.array_equal(np.array([a[q, d] for q, d in pairs]), np.array([v for _, v in ref]))
+
+
 @pytest.mark.parametrize("n_docs,radix,unfused", [(5000, False, False), (20000, False, False), (20000, True, False),
                                                    (20000, False, True)])
 def test_knn_prefilter_ids_exact(ft, opt, n_docs, radix, unfused):

@@ -1,6 +1,6 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests -x -q -m gpu --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
-python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-bash tools/profile_round.sh > gpurun_out/profile_round.log 2>&1
+python -m pytest tests/test_parity_gpu.py -x -q -k "chunk_pairs or knn or prefilter or quadtree or qt or full_size_sampled or subsets or tiny" > gpurun_out/pytest_small.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_small.log
+python tools/chunk_sweep.py reviews 0 > gpurun_out/stages.log 2>&1
+python tools/chunk_sweep.py stress 0 >> gpurun_out/stages.log 2>&1
+python tools/chunk_sweep.py text 0 >> gpurun_out/stages.log 2>&1
