@@ -916,15 +916,41 @@ __global__ void __launch_bounds__(1024) k_vocab(const uint32_t* __restrict__ doc
     for (int64_t i = threadIdx.x; i < nwords; i += blockDim.x) sbits[i] = 0u;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int64_t c = warp; c < n_cand; c += nw) {
-        const int64_t doc = cand[(int64_t)q * cand_ld + c];
-        // a negative candidate (padding / another shard's doc) has no rows; an index >= n is
-        // reported (NaN + FT_ERANGE) by the Flowtree kernels and contributes no rows here
-        if (doc < 0 || doc >= n) continue;
-        const uint32_t i0 = doc_off[doc], i1 = doc_off[doc + 1];
-        for (uint32_t i = i0 + lane; i < i1; i += 32) {
-            const uint32_t x = items[i].x & FTI_VOCAB_MASK;
-            atomicOr(&sbits[x >> 5], 1u << (x & 31));
+    // a warp takes KV docs at a time: lane j < KV loads doc j's id and offsets, then every lane
+    // loads its records of all KV docs (their loads in flight together — one doc at a time had
+    // made cand -> doc_off -> items one dependent chain per doc)
+    constexpr int KV = 4;
+    for (int64_t c0 = (int64_t)warp * KV; c0 < n_cand; c0 += (int64_t)nw * KV) {
+        uint32_t mi0 = 0, mi1 = 0;
+        if (lane < KV && c0 + lane < n_cand) {
+            const int64_t doc = cand[(int64_t)q * cand_ld + c0 + lane];
+            // a negative candidate (padding / another shard's doc) has no rows; an index >= n is
+            // reported (NaN + FT_ERANGE) by the Flowtree kernels and contributes no rows here
+            if (doc >= 0 && doc < n) { mi0 = doc_off[doc]; mi1 = doc_off[doc + 1]; }
+        }
+        uint32_t i0[KV], i1[KV], xs[KV][3];
+#pragma unroll
+        for (int j = 0; j < KV; j++) {
+            i0[j] = __shfl_sync(0xffffffffu, mi0, j);
+            i1[j] = __shfl_sync(0xffffffffu, mi1, j);
+#pragma unroll
+            for (int t = 0; t < 3; t++) {
+                const uint32_t i = i0[j] + lane + 32u * t;
+                xs[j][t] = i < i1[j] ? __ldg(&items[i].x) : FTI_EMPTY;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KV; j++) {
+#pragma unroll
+            for (int t = 0; t < 3; t++)
+                if (xs[j][t] != FTI_EMPTY) {
+                    const uint32_t x = xs[j][t] & FTI_VOCAB_MASK;
+                    atomicOr(&sbits[x >> 5], 1u << (x & 31));
+                }
+            for (uint32_t i = i0[j] + lane + 96u; i < i1[j]; i += 32) {   // supports beyond 96 items
+                const uint32_t x = __ldg(&items[i].x) & FTI_VOCAB_MASK;
+                atomicOr(&sbits[x >> 5], 1u << (x & 31));
+            }
         }
     }
     __syncthreads();
