@@ -378,12 +378,14 @@ struct QtArgs {
 struct QtThr {
     double t;
     float hi;
+    float cu;   // 2^{ℓ_root − D*} / U of the lane's query
 };
-__device__ __forceinline__ QtThr qt_thr(const QtArgs& a, int nqc, int cy) {
+__device__ __forceinline__ QtThr qt_thr(const QtArgs& a, int nqc, int cy, uint32_t U) {
     const int lane = threadIdx.x & 31;
-    QtThr r{0.0, 0.f};
+    QtThr r{0.0, 0.f, 0.f};
     if (a.thr && lane < nqc) {
         r.t = a.thr[(int64_t)(cy * QT_QC + lane) * a.thr_ld];
+        r.cu = U ? __fdiv_rn(a.pow2f, (float)U) : 0.f;
         r.hi = a.pow2f != 0.f ? __fmul_ru(__double2float_ru(r.t), 1.0f + 0x1p-18f) : __int_as_float(0x7f800000);
         if (r.t != r.t) r.hi = -1.f;   // NaN threshold: nothing passes (and the exact path agrees)
     }
@@ -410,9 +412,11 @@ __device__ __forceinline__ void qt_store(const QtArgs& a, const ChunkHdr& sh, in
         atomicOr(a.err, FTI_ERR_OVERFLOW);
     }
     if (a.thr && !bad) {
-        // FP32 screen: (float)num, (float)(U·W), the power of two and the reciprocal each round
-        // by ≤ 1 ulp (≤ 2^-21 relative in all), far inside the 2^-18 margin of th.hi
-        const float est = __fmul_rn(__fmul_rn(__ull2float_rn(num), a.pow2f), __frcp_rn(__ull2float_rn(Uq * W)));
+        // FP32 screen: (float)num, 2^k / U, the approximate reciprocal of W and two products each
+        // round by ≤ 2 ulp (≤ 2^-20 relative in all), inside the 2^-18 margin of th.hi
+        float rw;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"((float)W32));
+        const float est = __fmul_rn(__fmul_rn(__ull2float_rn(num), th.cu), rw);
         if (est > th.hi) return;
     }
     if (bad) {
@@ -446,7 +450,7 @@ __device__ __forceinline__ void qt_scan_dense(const QtArgs& a, const uint32_t* _
                                               const uint32_t* __restrict__ rank, const uint16_t* __restrict__ post,
                                               uint4* __restrict__ hq, const ChunkHdr& sh, int nqc, int cy) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const QtThr th = qt_thr(a, nqc, cy);
+    const QtThr th = qt_thr(a, nqc, cy, sh.U[threadIdx.x & 31]);
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
@@ -520,7 +524,7 @@ __device__ __forceinline__ void qt_scan_dense2(const QtArgs& a, const uint32_t* 
                                                int cy) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int na = (int)sa.nq, nb = (int)sb.nq;
-    const QtThr tha = qt_thr(a, na, cy), thb = qt_thr(a, nb, cy + 1);
+    const QtThr tha = qt_thr(a, na, cy, sa.U[lane]), thb = qt_thr(a, nb, cy + 1, sb.U[lane]);
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t Ua = sa.U[lane], Ub = sb.U[lane];
     const int64_t d0 = (int64_t)blockIdx.x * a.docs_per_cta;
@@ -595,7 +599,7 @@ __device__ __forceinline__ void qt_scan(const QtArgs& a, const uint32_t* __restr
                                         const uint16_t* __restrict__ idxs, const ChunkHdr& sh, int nqc, int cy) {
     const ChunkGeom& g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const QtThr th = qt_thr(a, nqc, cy);
+    const QtThr th = qt_thr(a, nqc, cy, sh.U[threadIdx.x & 31]);
     const uint32_t cmask = (uint32_t)g.cap - 1;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t U32 = sh.U[lane];
