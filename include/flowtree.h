@@ -194,6 +194,8 @@ uint64_t ft_launch_count(void);
  *   FT_OPT_PREFILTER_UNFUSED 1: ft_knn's prefilter writes every Quadtree value and then selects
  *                          (the fused sample-threshold scan is the default when n ≥ 32·m).
  *   FT_OPT_QT_PAIR_OFF     1: the Quadtree scan serves 32 queries per record pass (no chunk pairs).
+ *   FT_OPT_DIST_QMAJOR     1: exhaustive distance tables are built query by query (not tile-major
+ *                          with the A tile shared by consecutive work items).
  *   FT_OPT_DEBUG           bit mask of diagnostics printed to stderr: 1 distance-table role
  *                          clocks, 2 exact-W1 pivots, 4 selection paths, 8 scratch growth; and
  *                          16: ft_flowtree_flow fails (FT_ESTATE) unless the lane-per-pair kernel
@@ -211,7 +213,8 @@ typedef enum {
     FT_OPT_DEBUG = 9,
     FT_OPT_PREFILTER_UNFUSED = 10,
     FT_OPT_QT_PAIR_OFF = 11,
-    FT_NUM_OPTIONS = 12
+    FT_OPT_DIST_QMAJOR = 12,
+    FT_NUM_OPTIONS = 13
 } ft_option;
 ft_status ft_set_option(int32_t option, int64_t value);
 ft_status ft_get_option(int32_t option, int64_t* value);

@@ -243,6 +243,10 @@ struct DistArgs {
     int kz;                     // K bytes from kz on are zero padding in every row (round_up(d, 16))
     int nstage;                 // A ring depth
     int blk_outer;              // the ring holds a tile's whole K range (nstage == nks)
+    // tile-major order (exhaustive tables: every query's rows are all vocab ids): item
+    // tile·GQ + gbase[q] + g, so consecutive items share their A tile and its copy is skipped
+    int tmajor;
+    int32_t* gbase;             // [nq + 1] exclusive prefix of the queries' column groups (GQ = gbase[nq])
 };
 
 __device__ unsigned long long g_dbg[16];
@@ -431,6 +435,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
         uint32_t eph = 0;
         bool first = true;
         const uint64_t pol = FTD_L2POL ? l2_policy_last() : 0ull;
+        int prev_tile = -1;
         for (int64_t w = w_begin; w < w_end; w++) {
             const int8_t* src[RG];
 #pragma unroll
@@ -438,10 +443,14 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
                 src[rg] = a.Xq + (px[rg] >= 0 ? (int64_t)px[rg] : a.N) * rstride + 16 * gq;
                 if (w + 1 < w_end && grp_ok(rg)) px[rg] = a.wrow[(w + 1) * TM + (warp + NCW * rg) * 8 + rl];
             }
+            // tile-major order: the ring still holds this tile (every stage keeps its slot)
+            const int tile = a.tmajor ? a.wdesc[w].y : -1;
+            const bool reuse = kfixed && a.tmajor && tile == prev_tile;
+            prev_tile = tile;
             for (int c = 0; c < a.nks; c++) {
                 if (!first) TW(0, mbar_wait(&empty[s], eph));
                 const uint32_t st = abase + (uint32_t)s * STAGE_BYTES;
-                const bool live = !kfixed || KS * c + 16 * gq < a.kz;   // not an all-zero padding granule
+                const bool live = !reuse && (!kfixed || KS * c + 16 * gq < a.kz);   // not an all-zero padding granule
 #pragma unroll
                 for (int p = 0; p < NL; p++)
 #pragma unroll
@@ -758,8 +767,8 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
 // next slot, the algorithmic flops Σ_q 2 · rows_q · s_q · d (one multiply-add per coordinate of
 // every entry).
 __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned long long* units) {
-    __shared__ int tmp_t[32], tmp_b[32];
-    int64_t tacc = 0, bacc = 0;
+    __shared__ int tmp_t[32], tmp_b[32], tmp_g[32];
+    int64_t tacc = 0, bacc = 0, gacc = 0;
     unsigned long long bytes = 0, flops = 0;
     for (int q0 = 0; q0 < a.nq; q0 += blockDim.x) {
         const int q = q0 + threadIdx.x;
@@ -775,10 +784,13 @@ __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned 
             const int last = s - NGRP * (G - 1);
             bsz = s > 0 ? (NL * a.kpad / 16) * (NGRP * (G - 1) + ((last + 15) & ~15)) : 0;
         }
-        int tt, bt;
+        int tt, bt, gt;
         const int tex = fti_block_exclusive_sum(items, tmp_t, &tt);
         const int bex = fti_block_exclusive_sum(bsz, tmp_b, &bt);
+        const int ng = s > 0 ? (s + NGRP - 1) / NGRP : 0;
+        const int gex = fti_block_exclusive_sum(ng, tmp_g, &gt);
         if (q < a.nq) {
+            if (a.gbase) a.gbase[q] = (int32_t)(gacc + gex);
             a.tile_base[q] = tacc + tex;
             a.qinfo[q] = make_uint2((uint32_t)(bacc + bex), (uint32_t)s);
             if (s > 0) {
@@ -788,9 +800,13 @@ __global__ void __launch_bounds__(1024) k_tile_plan(DistArgs a, int d, unsigned 
         }
         tacc += tt;
         bacc += bt;
+        gacc += gt;
         __syncthreads();
     }
-    if (threadIdx.x == 0) a.tile_base[a.nq] = tacc;
+    if (threadIdx.x == 0) {
+        a.tile_base[a.nq] = tacc;
+        if (a.gbase) a.gbase[a.nq] = (int32_t)gacc;
+    }
     if (units && bytes) atomicAdd(units, bytes);
     if (units && flops) atomicAdd(units + (FT_PROF_DIST_FLOPS - FTI_ST_DIST), flops);
 }
@@ -803,8 +819,10 @@ __global__ void __launch_bounds__(TM) k_tiles(DistArgs a) {
     const int64_t t0 = a.tile_base[q], t1 = a.tile_base[q + 1];
     const int64_t nrows = a.rowcnt ? (int64_t)a.rowcnt[q] : a.rows_cap;
     const int64_t tiles = (nrows + TM - 1) / TM;
-    for (int64_t w = t0 + blockIdx.y; w < t1; w += gridDim.y) {
-        const int64_t g = (w - t0) / tiles, tile = (w - t0) - g * tiles;
+    const int64_t GQ = a.tmajor ? (int64_t)a.gbase[a.nq] : 0;
+    for (int64_t wl = t0 + blockIdx.y; wl < t1; wl += gridDim.y) {
+        const int64_t g = (wl - t0) / tiles, tile = (wl - t0) - g * tiles;
+        const int64_t w = a.tmajor ? tile * GQ + a.gbase[q] + g : wl;
         const int64_t row = tile * TM + threadIdx.x;
         int32_t xid = -1;
         if (row < nrows) xid = a.rows ? a.rows[(int64_t)q * a.rows_cap + row] : (int32_t)row;
@@ -1063,6 +1081,7 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     const int G = (L.smax + NGRP - 1) / NGRP;
     a.ny_ld = G * NGRP;
     const int64_t tmax = (int64_t)nq * G * ((rows_cap + TM - 1) / TM);
+    if ((e = ds->s_gbase.reserve((size_t)(nq + 1) * 4)) != cudaSuccess) return e;
     if ((e = ds->s_bsplit.reserve((size_t)nq * G * NL * NGRP * a.kpad)) != cudaSuccess) return e;
     if ((e = ds->s_ny.reserve((size_t)nq * a.ny_ld * 8)) != cudaSuccess) return e;
     if ((e = ds->s_tiles.reserve((size_t)(nq + 1) * 8)) != cudaSuccess) return e;
@@ -1082,6 +1101,9 @@ cudaError_t fti_launch_dist_table(ft_dataset* ds, const QueryLayout& L, const ui
     a.blk_outer = (!FTD_KOUTER && nstage >= a.nks) ? 1 : 0;
     if (!a.blk_outer && !FTD_KOUTER) nstage = std::min(nstage, 4);
     a.nstage = nstage;
+    a.gbase = ds->s_gbase.as<int32_t>();
+    a.tmajor = (d_rows == nullptr && d_rowcnt == nullptr && a.blk_outer && nstage == a.nks &&
+                !fti_opt(FT_OPT_DIST_QMAJOR)) ? 1 : 0;
     const size_t smem = dist_smem(nstage, a.kpad);
     const bool dbg = (fti_opt(FT_OPT_DEBUG) & FTI_DBG_DIST) != 0;
     auto kern = dbg ? k_dist_i8<true> : k_dist_i8<false>;

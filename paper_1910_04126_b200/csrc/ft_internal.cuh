@@ -184,6 +184,7 @@ struct ft_dataset {
     // fused prefilter (fti_launch_prefilter): sample doc ids, sample values, thresholds, lists
     DevBuf s_pf_samp, s_pf_sval, s_pf_tval, s_pf_cnt, s_pf_cval, s_pf_cid, s_pf_bad, s_pf_flag;
     DevBuf s_chunkd2;   // Quadtree chunk-pair dense structures (ft_qt.cu)
+    DevBuf s_gbase;     // distance-table work list: per-query column-group prefix (ft_dist.cu)
     int64_t pf_ns = -1;
 };
 

@@ -382,7 +382,7 @@ extern "C" void ft_dataset_free(ft_dataset* ds) {
     if (ds->prof_units) cudaFree(ds->prof_units);
     DevBuf* bufs[] = {&ds->s_qoff, &ds->s_qids, &ds->s_qw, &ds->s_qblock, &ds->s_docs, &ds->s_vals, &ds->s_vals2,
                       &ds->s_cand, &ds->s_outid, &ds->s_outval, &ds->s_map, &ds->s_rows, &ds->s_rowcnt,
-                      &ds->s_table, &ds->s_flow, &ds->s_flowcnt, &ds->s_vlist, &ds->s_chunk, &ds->s_rowbase, &ds->s_bsplit, &ds->s_ny, &ds->s_tiles, &ds->s_qinfo, &ds->s_wdesc, &ds->s_wrow, &ds->s_sel, &ds->s_chunkd, &ds->s_fblist, &ds->s_fbcnt, &ds->s_topk, &ds->s_pitch, &ds->s_chunkd2};
+                      &ds->s_table, &ds->s_flow, &ds->s_flowcnt, &ds->s_vlist, &ds->s_chunk, &ds->s_rowbase, &ds->s_bsplit, &ds->s_ny, &ds->s_tiles, &ds->s_qinfo, &ds->s_wdesc, &ds->s_wrow, &ds->s_sel, &ds->s_chunkd, &ds->s_fblist, &ds->s_fbcnt, &ds->s_topk, &ds->s_pitch, &ds->s_chunkd2, &ds->s_gbase};
     for (DevBuf* b : bufs) b->release();
     delete ds;
 }

@@ -34,8 +34,8 @@ FT_NUM_STAGES = 7
 # ft_set_option keys (include/flowtree.h)
 (FT_OPT_VOCAB_HASH, FT_OPT_WARP_ONLY, FT_OPT_QT_HASH, FT_OPT_SELECT_RADIX, FT_OPT_EXACT_START_NW,
  FT_OPT_TABLE_CHUNK, FT_OPT_TABLE_BUDGET_MB, FT_OPT_QT_WAVES, FT_OPT_FTD_CARVEOUT, FT_OPT_DEBUG,
- FT_OPT_PREFILTER_UNFUSED, FT_OPT_QT_PAIR_OFF) = range(12)
-FT_NUM_OPTIONS = 12
+ FT_OPT_PREFILTER_UNFUSED, FT_OPT_QT_PAIR_OFF, FT_OPT_DIST_QMAJOR) = range(13)
+FT_NUM_OPTIONS = 13
 FT_PROF_DIST_FLOPS = FT_NUM_STAGES   # ft_profile_units slot: distance-table algorithmic flops
 
 

@@ -232,6 +232,25 @@ def test_vocab_hash_path_matches_bitmap(ft, opt):
         assert np.array_equal(f_a[key], f_b[key])
 
 
+@pytest.mark.parametrize("name,n_docs,nq", [("text", 1500, 37), ("reviews", 2500, 9), ("stress", 3000, 70)])
+def test_tile_major_exhaustive_table_bit_identical(ft, opt, name, n_docs, nq):
+    """Exhaustive distance tables are built tile-major (every query's rows are all vocab ids, so
+    consecutive work items share their A tile and skip its copy); the table entries are the same
+    exact-integer distances as the query-major order (FT_OPT_DIST_QMAJOR), so every Flowtree value
+    is bit-identical; and a sample against the oracle."""
+    wl = get_workload(name, n_docs=n_docs, n_queries=nq)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    a = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    opt("FT_OPT_DIST_QMAJOR")
+    b = ds.flowtree(wl.q_off, wl.q_ids, wl.q_w)
+    assert np.array_equal(a, b)
+    rng = np.random.default_rng(4)
+    pairs = [(int(q), int(d)) for q, d in zip(rng.integers(0, wl.nq, 40), rng.integers(0, wl.n, 40))]
+    ref = _oracle_all(T, wl, "ft", pairs)
+    assert_ft_close([a[q, d] for q, d in pairs], ref, f"{name} tile-major FT")
+
+
 @pytest.mark.parametrize("name,nq", [("text", 40), ("reviews", 70)])
 def test_chunked_flowtree_matches_warp_kernel(ft, opt, name, nq):
     """Exhaustive scoring runs the lane-per-pair kernel k_ftd (pairs sharing an M-node are listed
