@@ -33,7 +33,10 @@ namespace {
 #define FTD_MINB 3         // CTAs per SM the register budget allows
 #endif
 constexpr int DW = 8;      // warps per CTA
-constexpr int DCAP = 32;   // shared ids per pair held in the per-lane queue
+#ifndef FTD_DCAP
+#define FTD_DCAP 32
+#endif
+constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
 constexpr int DQN = DCAP + 2;            // queue slots per lane: entries + two sentinels
 constexpr int DRB = 8;     // merge steps per gather batch
 constexpr uint32_t DQ_END = 0xFFFFu;     // queue sentinel: i = j = 255 never matches (s, sq ≤ 254)

@@ -1,9 +1,6 @@
 set -u
 mkdir -p gpurun_out
-for v in h03 h045 h08; do
-  FT_LIB=$PWD/build/variants/$v/libflowtree_b200.so python tools/chunk_sweep.py reviews 0 > gpurun_out/hv_$v.log 2>&1
-  FT_LIB=$PWD/build/variants/$v/libflowtree_b200.so python tools/chunk_sweep.py stress 0 >> gpurun_out/hv_$v.log 2>&1
-done
-FT_OPT=1 python -c "
-import sys; sys.argv=['x','reviews','0']
-" 
+python -m pytest tests -x -q -m gpu --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+bash tools/profile_round.sh > gpurun_out/profile_round.log 2>&1
