@@ -34,7 +34,7 @@ namespace {
 #endif
 constexpr int DW = 8;      // warps per CTA
 #ifndef FTD_DCAP
-#define FTD_DCAP 32
+#define FTD_DCAP 48
 #endif
 constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
 constexpr int DQN = DCAP + 2;            // queue slots per lane: entries + two sentinels

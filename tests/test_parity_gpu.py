@@ -271,7 +271,7 @@ def test_chunked_flowtree_matches_warp_kernel(ft, opt, name, nq):
                                            ("stress", 5, "lists")])
 def test_lane_per_pair_flowtree_matches_other_kernels(ft, opt, name, nq, mode):
     """The lane-per-pair kernel (k_ftd: 32 pairs of one query per warp, pairs with a common M-node
-    or more than 32 shared ids listed for the warp kernel) against the warp kernel for every pair
+    or more than 48 shared ids listed for the warp kernel) against the warp kernel for every pair
     (FT_OPT_WARP_ONLY).  Candidate
     lists (mode "lists") hold repeats and a ragged tail, as the pipeline's top-m rows do."""
     wl = get_workload(name, n_docs=3000, n_queries=nq)
