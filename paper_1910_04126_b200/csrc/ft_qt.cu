@@ -854,9 +854,10 @@ cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* 
     return cudaGetLastError();
 }
 
-// CTAs per SM slot over a full scan (measured: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews
-// batch); FT_OPT_QT_WAVES tunes it
-int qt_waves() { return fti_opt(FT_OPT_QT_WAVES) > 0 ? (int)fti_opt(FT_OPT_QT_WAVES) : 8; }
+// CTAs per SM slot over a full scan (single chunks: 4 → 2.48 ms, 8 → 2.19, 12 → 2.34 ms per reviews
+// batch; chunk pairs: 4 → 2.17, 6 → 2.41, 8 → 2.22, 16 → 2.37 ms, stress 3.76 / 3.79 / 3.84 / 4.00
+// ms); FT_OPT_QT_WAVES tunes it
+int qt_waves() { return fti_opt(FT_OPT_QT_WAVES) > 0 ? (int)fti_opt(FT_OPT_QT_WAVES) : 4; }
 
 // flags [nq] from a row list {count, rows...}
 __global__ void k_rows_to_flags(const int* __restrict__ list, uint32_t* __restrict__ flag, int32_t nq) {

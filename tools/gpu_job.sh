@@ -1,3 +1,4 @@
 set -u
 mkdir -p gpurun_out
-python -m pytest tests/test_parity_gpu.py -x -q -k "lane_per_pair or chunked or flow_export or degenerate or subsets or full_size_sampled or tile_major or bounds_checked" > gpurun_out/pytest_small.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_small.log
+python tools/opt_sweep.py reviews FT_OPT_QT_WAVES 4 6 8 12 16 > gpurun_out/waves.log 2>&1
+python tools/opt_sweep.py stress FT_OPT_QT_WAVES 4 6 8 12 16 >> gpurun_out/waves.log 2>&1
