@@ -190,7 +190,7 @@ uint64_t ft_launch_count(void);
  *   FT_OPT_TABLE_BUDGET_MB > 0: distance-table bytes per chunk (default: 1/4 of free HBM at the
  *                          dataset's first Flowtree call, at most 48 GB).
  *   FT_OPT_QT_WAVES        > 0: CTA waves per SM slot of the Quadtree launch (default 4).
- *   FT_OPT_FTD_CARVEOUT    1..100: k_ftd shared-memory carveout percent (0: sized for 3 CTAs/SM).
+ *   FT_OPT_FTD_CARVEOUT    1..100: k_ftd shared-memory carveout percent (0: sized for the kernel's CTAs per SM: 3, or 2 with compact tables).
  *   FT_OPT_PREFILTER_UNFUSED 1: ft_knn's prefilter writes every Quadtree value and then selects
  *                          (the fused sample-threshold scan is the default when n ≥ 32·m).
  *   FT_OPT_QT_PAIR_OFF     1: the Quadtree scan serves 32 queries per record pass (no chunk pairs).
