@@ -44,7 +44,10 @@ constexpr int DW = 8;      // warps per CTA
 #endif
 constexpr int DCAP = FTD_DCAP;   // shared ids per pair held in the per-lane queue
 constexpr int DQN = DCAP + 2;            // queue slots per lane: entries + two sentinels
-constexpr int DRB = 8;     // merge steps per gather batch
+#ifndef FTD_DRB
+#define FTD_DRB 8
+#endif
+constexpr int DRB = FTD_DRB;   // merge steps per gather batch
 constexpr uint32_t DQ_END = 0xFFFFu;     // queue sentinel: i = j = 255 never matches (s, sq ≤ 254)
 
 struct DArgs {
