@@ -332,7 +332,7 @@ __global__ void FTD_KATTR k_dist_i8(DistArgs a) {
         // groups (3 per pair: units 0-3 of each group, then units 4-5 of both), in two halves of 6
         // slots that are double buffered in registers.  Unit k of a row = limb k / 2, 32-byte half
         // k % 2 of the stage's 64 coordinates.
-        static_assert(NCOPY == 64, "LDG copy path: two copy warps");
+        static_assert(!FTD_LDGCP || NCOPY == 64, "LDG copy path: two copy warps");
         const int cw = warp;
         const uint32_t abase = smem_u32(aring);
         const size_t rstride = (size_t)a.nks * ROWB;

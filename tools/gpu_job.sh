@@ -1,9 +1,10 @@
 set -u
 mkdir -p gpurun_out
-: > gpurun_out/drb.log
-for v in base drb12 drb16 drb12m3; do
-  echo "== $v" >> gpurun_out/drb.log
+: > gpurun_out/ncopy.log
+for v in base c96 c128 c128e4; do
+  echo "== $v" >> gpurun_out/ncopy.log
   L=""; [ "$v" != base ] && L="FT_LIB=$PWD/build/variants/$v/libflowtree_b200.so"
-  env $L python tools/ft_exh.py reviews 64 >> gpurun_out/drb.log 2>&1
-  env $L python tools/chunk_sweep.py reviews 0 >> gpurun_out/drb.log 2>&1
+  env $L timeout 300 python tools/chunk_sweep.py reviews 0 >> gpurun_out/ncopy.log 2>&1
+  env $L timeout 300 python tools/chunk_sweep.py stress 0 >> gpurun_out/ncopy.log 2>&1
+  env $L timeout 300 python tools/ft_exh.py reviews 64 >> gpurun_out/ncopy.log 2>&1
 done
