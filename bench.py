@@ -198,6 +198,14 @@ def measure_configs(ft, workloads, torch, dev, stream, peak, flush, names):
         ov = torch.empty((nq, k), dtype=torch.float64, device=dev)
         reps = 2 if name == "image" else 3
         knn_ms = timed(lambda: ds.knn(wl.q_off, qi, qw, k, m, out_ids=oi, out_val=ov, stream=stream), reps)
+        # end to end through the C ABI: queries from pinned host memory, answers back to pinned host
+        # memory (the call copies both ways on the stream; the events bracket the copies)
+        qi_pin = torch.from_numpy(wl.q_ids.copy()).pin_memory()
+        qw_pin = torch.from_numpy(wl.q_w.view(np.int32).copy()).pin_memory().view(torch.uint32)
+        oi_pin = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+        ov_pin = torch.empty((nq, k), dtype=torch.float64).pin_memory()
+        e2e_ms = timed(lambda: ds.knn(wl.q_off, qi_pin, qw_pin, k, m, out_ids=oi_pin, out_val=ov_pin, stream=stream),
+                       reps)
         # Quadtree over all docs for the whole batch (8 B per doc tree node + 16 B per pair)
         out_qt = torch.empty((nq, n), dtype=torch.float64, device=dev)
         qt_ms = timed(lambda: ds.quadtree(wl.q_off, qi, qw, out=out_qt, stream=stream), 3)
@@ -225,6 +233,8 @@ def measure_configs(ft, workloads, torch, dev, stream, peak, flush, names):
         out[name] = {
             "n": n, "N": int(wl.X.shape[0]), "d": int(wl.X.shape[1]), "queries": nq, "k": k, "prefilter_m": m,
             "knn_ms_per_batch": knn_ms, "knn_queries_per_s": nq / (knn_ms / 1e3),
+            "e2e_queries_per_s": nq / (e2e_ms / 1e3),
+            "e2e_h2d_bytes": 8 * (nq + 1) + 4 * len(wl.q_ids) + 4 * len(wl.q_w), "e2e_d2h_bytes": nq * k * 16,
             "qt_pairs_per_s": qt_rate, "qt_bytes_per_pair": qt_bpp, "qt_frac_hbm": qt_rate * qt_bpp / 1e9 / peak,
             "ft_queries": nqf, "ft_pairs_per_s": ft_rate, "ft_bytes_per_pair": ft_bpp,
             "ft_frac_hbm": ft_rate * ft_bpp / 1e9 / peak, "ft_dist_table_ms": d_ms,
