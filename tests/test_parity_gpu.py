@@ -584,6 +584,36 @@ def test_prefilter_fused_overflow_fallback(ft):
     assert set(got[0].tolist()) == set(range(m))        # the tied copies, smallest ids first
 
 
+def test_prefilter_overflow_fallback_in_a_chunk_pair(ft):
+    """The same overflow inside a 64-query chunk pair (40 queries: chunks of 32 + 8 share one CTA
+    row; the overflowing query is #35, in the second chunk): the fallback pass re-scans the pair's
+    flagged rows only, and the ordinary rows keep their list results."""
+    base = get_workload("reviews", n_docs=2001, n_queries=40)
+    T = oracle_tree(base)
+    src = [0] * 36000 + list(range(1, 2001))
+    docs = [base.doc(d) for d in src]
+    doc_off = np.zeros(len(src) + 1, np.int64)
+    doc_off[1:] = np.cumsum([len(i) for i, _ in docs])
+    ids = np.concatenate([i for i, _ in docs]).astype(np.int32)
+    w = np.concatenate([x for _, x in docs]).astype(np.uint32)
+    qs = [base.query(j) for j in range(40)]
+    qs[35] = base.doc(0)
+    q_off = np.zeros(41, np.int64)
+    q_off[1:] = np.cumsum([len(i) for i, _ in qs])
+    q_ids = np.concatenate([i for i, _ in qs]).astype(np.int32)
+    q_w = np.concatenate([x for _, x in qs]).astype(np.uint32)
+    ix = ft.Index(base.X, seed=base.tree_seed, max_depth=base.max_depth)
+    ds = ft.Dataset(ix, doc_off, ids, w)
+    m = 300
+    got, vals = ds.knn(q_off, q_ids, q_w, m, m)
+    for q in (0, 31, 35, 39):
+        b, bw = qs[q]
+        qd = pmap(lambda d: T.qt(*base.doc(d), b, bw)[1], range(2001))
+        top = sorted(range(len(src)), key=lambda i: (qd[src[i]], i))[:m]
+        assert set(got[q].tolist()) == set(top), f"query {q}"
+    assert set(got[35].tolist()) == set(range(m))
+
+
 def test_knn_padding_and_errors(ft):
     wl = get_workload("tiny", n_docs=7)
     ix, ds = _setup(ft, wl)
