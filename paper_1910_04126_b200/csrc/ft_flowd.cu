@@ -47,6 +47,10 @@ constexpr int DQN = DCAP + 2;            // queue slots per lane: entries + two 
 #ifndef FTD_DRB
 #define FTD_DRB 8
 #endif
+#ifndef FTD_PREV
+#define FTD_PREV 1       // pre-pass reads the doc records with 32-byte loads (0: one 4-byte load per record)
+#endif
+
 constexpr int DRB = FTD_DRB;   // merge steps per gather batch
 constexpr uint32_t DQ_END = 0xFFFFu;     // queue sentinel: i = j = 255 never matches (s, sq ≤ 254)
 
@@ -191,6 +195,37 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
         // shared ids, in vocab order: {i | j << 8}, then two sentinels
         int nc = 0;
         if (active) {
+#if FTD_PREV
+            // 32-byte loads of four records each from the aligned-down start: a lane's request is one
+            // sector whatever its width, and the L1 serves about one lane request per clock
+            // (exhaustive reviews 2.88 -> 2.62 ms, text 0.537 -> 0.505, stress 6.00 -> 5.67)
+            const int ia = -(int)(i0 & 3u);
+            for (int i = ia; i < s; i += 8) {
+                uint32_t xv[8];
+                {
+                    uint32_t r[16];
+                    const uint2* p = a.items + i0 + i;
+                    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                                 : "l"(p));
+                    asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                                 : "l"(p + 4));
+#pragma unroll
+                    for (int u = 0; u < 8; u++) xv[u] = r[2 * u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const uint32_t x = xv[u] & FTI_VOCAB_MASK;
+                    const uint32_t bw = qbits[x >> 5], bm = 1u << (x & 31);
+                    if (i + u >= 0 && i + u < s && (bw & bm)) {
+                        const uint32_t j = qrank[x >> 5] + __popc(bw & (bm - 1u));
+                        if (nc < DCAP) myq[nc * 32] = (uint16_t)((uint32_t)(i + u) | (j << 8));
+                        nc++;
+                    }
+                }
+            }
+#else
             for (int i = 0; i < s; i += 8) {
                 uint32_t xv[8];
 #pragma unroll
@@ -206,6 +241,7 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                     }
                 }
             }
+#endif
             if (nc <= DCAP) {
                 myq[nc * 32] = (uint16_t)DQ_END;
                 myq[(nc + 1) * 32] = (uint16_t)DQ_END;
@@ -345,7 +381,8 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                     // raw records loaded three advances before use (x3..x5: items i+3..i+5): the
                     // record load's latency had been the merge's largest stall
                     // (a predicated inline-PTX load straight into x5's register, to avoid the select
-                    // on the fresh load: 2.89 -> 3.10 ms exhaustive, not kept)
+                    // on the fresh load: 2.89 -> 3.10 ms exhaustive, not kept; two records per 16-byte
+                    // load on every other advance: 2.88 -> 3.55 ms, not kept)
                     if (ad) {
                         x2 = x3 & FTI_VOCAB_MASK;
                         x3 = x4;
