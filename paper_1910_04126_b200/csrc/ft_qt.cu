@@ -845,7 +845,9 @@ cudaError_t qt_scan(ft_dataset* ds, const QtPlan& P, int32_t nq, const int64_t* 
     a.err = ds->err_dev;
     const int64_t target = (int64_t)148 * P.ctas_per_sm * waves;
     const int64_t rows_y = P.dg.cap2 > 0 ? (P.nchunks + 1) / 2 : P.nchunks;
-    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, (target + rows_y - 1) / rows_y));
+    // whole waves only: the grid never exceeds `target` CTAs (rounding up had given the 1/32-sample
+    // scan 160 CTAs on 148 SMs — a second wave of 12)
+    int64_t bx = std::max<int64_t>(1, std::min<int64_t>((n_docs + 31) / 32, target / rows_y));
     a.docs_per_cta = (n_docs + bx - 1) / bx;
     bx = (n_docs + a.docs_per_cta - 1) / a.docs_per_cta;
     const int gy = a.pair ? (P.nchunks + 1) / 2 : P.nchunks;
