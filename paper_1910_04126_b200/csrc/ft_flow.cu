@@ -681,6 +681,7 @@ cudaError_t fti_launch_ft(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
             a.fb_cap = n_docs;
             bx = std::max<int64_t>(1, std::min<int64_t>(32, (148 * 4 + nq - 1) / nq));
         } else if (e != cudaErrorNotSupported) {
+            if (fti_opt(FT_OPT_DEBUG)) fprintf(stderr, "fti_launch_ft: k_ftd launch failed: %s\n", cudaGetErrorString(e));
             return e;
         }
     }

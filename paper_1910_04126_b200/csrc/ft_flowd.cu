@@ -58,6 +58,7 @@ struct DArgs {
     const uint32_t* doc_off;
     const uint2* items;
     const uint32_t* Wd;
+    int64_t nnz;               // records in items (followed by 8 zero records of padding)
     const uint32_t* mn_off;
     const uint4* mnodes;
     const uint16_t* mlists;
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                 bool multi_shared = false;
                 for (uint32_t t = 0; t < rec.z; t++) {
                     const uint32_t ii = a.mlists[rec.y + t];
+                    FTI_ASSERT(ii < (uint32_t)s);
                     const uint32_t xv = a.items[i0 + ii].x;
                     const uint32_t x = xv & FTI_VOCAB_MASK;
                     uint32_t m = dw[2 * ii] * U;
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                 }
                 for (uint32_t t = 0; t < qe.z && dsum && !multi_shared; t++) {
                     const uint32_t jj = gml[qe.y + t];
+                    FTI_ASSERT(qe.y + t < hdr->n_ml && jj < sq);
                     uint32_t m = qitem[jj].y * W;
                     for (int c = 0; c < nc; c++) {
                         const uint32_t e = myq[c * 32];
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
         const bool to_list = dp < a.n_docs && !active && s > 0 && qok && doc >= 0 && doc < a.n;
         if (to_list) {
             const uint32_t pos = atomicAdd(&a.fb_cnt[q], 1u);
+            FTI_ASSERT((int64_t)pos < a.fb_cap);
             a.fb_list[(int64_t)q * a.fb_cap + pos] = (uint32_t)dp;
         }
         const bool scored = active;
@@ -331,8 +335,8 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
             // doc's end into valid records: the items array carries 8 zero records of padding).  A
             // shared doc item's leftover is U − min(U, W) (its flag comes from the query bitmap); the
             // query side takes its shared items from the queue (qh = query index of the next one).
-            // Past a side's last item its boundary grows once beyond the total W·U (no overflow:
-            // W·U ≤ 65535²) and never matches again; the merge ends when both sides are done.
+            // Both sides carry the same total residual, so the merge ends when either side's last
+            // item is consumed (no overflow: W·U ≤ 65535²).
             const uint32_t mm = U < W ? U : W, Ud = U - mm, Wq = W - mm;
             auto dres = [&](uint32_t x) { return ((qbits[x >> 5] >> (x & 31)) & 1u) ? Ud : U; };
             int i = 0, j = 0;
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                         x2 = x3 & FTI_VOCAB_MASK;
                         x3 = x4;
                         x4 = x5;
+                        FTI_ASSERT(pn - a.items < a.nnz + 8);
                         x5 = pn->x;
                     }
                     pn += ad;
@@ -399,7 +404,13 @@ __global__ void __launch_bounds__(DW * 32, MAP ? FTD_MINB_MAP : FTD_MINB) k_ftd(
                     qh = hq ? ne >> 8 : qh;
                     qaddr += hq ? 64u : 0u;
                     j += aq;
-                    active = active && (i < s || j < (int)sq);
+                    // the two sides carry the same total residual, so when either runs out every
+                    // unit is matched: stop.  (Stopping only when BOTH were done let a finished doc
+                    // side keep stepping while the record after the doc's last was a shared id
+                    // with leftover U − min(U, W) = 0 — its boundary never grew, `ad` fired on
+                    // every remaining query step and pn ran up to s_q records past the doc: beyond
+                    // the array's padding after the dataset's last doc.  All those steps had η = 0.)
+                    active = active && i < s && j < (int)sq;
                 }
                 if (!EXPORT) {
                     float part = 0.f;
@@ -549,6 +560,7 @@ cudaError_t fti_launch_ftd(ft_dataset* ds, const QueryLayout& L, const uint8_t* 
     if ((e = ds->s_fbcnt.reserve((size_t)nq * 4)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(ds->s_fbcnt.p, 0, (size_t)nq * 4, st)) != cudaSuccess) return e;
     a.doc_off = ds->doc_off; a.items = ds->items; a.Wd = ds->W;
+    a.nnz = ds->nnz;
     a.mn_off = ds->mn_off; a.mnodes = ds->mnodes; a.mlists = ds->mlists;
     a.qblock = d_qblock; a.L = L;
     a.docs = d_docs; a.docs_ld = docs_ld; a.n_docs = n_docs; a.n = ds->n;

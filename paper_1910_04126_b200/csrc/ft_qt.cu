@@ -48,11 +48,12 @@ struct ChunkHdr {
     unsigned long long B[QT_QC];
 };
 
-ChunkGeom chunk_geom(const ft_dataset* ds, const QueryLayout& L) {
+// geometry of a chunk that holds up to qc (≤ QT_QC) queries
+ChunkGeom chunk_geom(const ft_dataset* ds, const QueryLayout& L, int qc) {
     ChunkGeom g;
     const int64_t per_q = std::min<int64_t>((int64_t)L.smax * std::max(1, ds->ix->d_star), ds->ix->M);
-    g.umax = (int)std::min<int64_t>(std::min<int64_t>((int64_t)QT_QC * per_q, ds->ix->M), 65535);
-    g.pmax = (int)((int64_t)QT_QC * per_q);
+    g.umax = (int)std::min<int64_t>(std::min<int64_t>((int64_t)qc * per_q, ds->ix->M), 65535);
+    g.pmax = (int)((int64_t)qc * per_q);
     g.cap = fti_pow2_at_least(std::max(64, g.umax + g.umax / 4 + 1));
     g.ucap_s = (std::min(g.umax, QT_UCAP_S) + 7) & ~7;   // multiples of 8 keep the u16 idx array 16-B aligned
     g.pcap_s = (std::min(g.pmax, QT_PCAP_S) + 7) & ~7;
@@ -65,6 +66,23 @@ ChunkGeom chunk_geom(const ft_dataset* ds, const QueryLayout& L) {
     g.off_post = o; o = up(o + 4ull * g.pmax);
     g.stride = o;
     return g;
+}
+
+// the chunk's node hash (keys + dense indices, 6 bytes per slot) is always staged in shared memory,
+// by the builder next to the masks/offsets and by the scan next to the staged postings
+constexpr int QT_CAP_MAX = 16384;
+bool chunk_fits(const ChunkGeom& g) {
+    return g.cap <= QT_CAP_MAX && 6ull * g.cap + 8ull * g.umax <= 220 * 1024;
+}
+
+// queries per chunk for this batch: QT_QC unless the worst-case node union of 32 large-support
+// queries on a deep tree would not fit the shared-memory hash; then the largest power of two that
+// does (the batch is scored in sub-batches of that many queries, one partly filled chunk each).
+// Within the documented limits (support × depth ≤ 8192) one query always fits.
+int qt_fit_queries(const ft_dataset* ds, const QueryLayout& L) {
+    for (int qc = QT_QC; qc >= 1; qc >>= 1)
+        if (chunk_fits(chunk_geom(ds, L, qc))) return qc;
+    return 0;
 }
 
 __device__ __forceinline__ int probe_slot(const uint32_t* keys, uint32_t mask, uint32_t node) {
@@ -769,12 +787,12 @@ struct QtPlan {
 
 cudaError_t qt_prepare(ft_dataset* ds, const QueryLayout& L, const uint8_t* d_qblock, int32_t nq, cudaStream_t st,
                        QtPlan& P) {
-    P.g = chunk_geom(ds, L);
+    P.g = chunk_geom(ds, L, std::min<int>(nq, QT_QC));
     P.nchunks = (nq + QT_QC - 1) / QT_QC;
+    if (!chunk_fits(P.g)) return cudaErrorInvalidConfiguration;   // callers split such batches (qt_fit_queries)
     cudaError_t e = ds->s_chunk.reserve(P.g.stride * (size_t)P.nchunks);
     if (e != cudaSuccess) return e;
     size_t smem_c = 4ull * P.g.cap + 8ull * P.g.umax + 2ull * P.g.cap;
-    if (smem_c > 220 * 1024) return cudaErrorInvalidConfiguration;   // query batch too large for one chunk
     e = cudaFuncSetAttribute(k_qt_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
     if (e != cudaSuccess) return e;
     k_qt_chunk<<<P.nchunks, 1024, smem_c, st>>>(d_qblock, L, nq, P.g, ds->s_chunk.as<uint8_t>(), ds->err_dev);
@@ -876,6 +894,16 @@ cudaError_t fti_launch_qt(ft_dataset* ds, const QueryLayout& L, const uint8_t* d
                           cudaStream_t st) {
     (void)docs_ld;   // the Quadtree stage always scores one doc list shared by the batch
     if (nq <= 0 || n_docs <= 0) return cudaSuccess;
+    const int qc = qt_fit_queries(ds, L);
+    if (qc <= 0) return cudaErrorInvalidConfiguration;
+    if (qc < QT_QC && nq > qc) {   // large supports on a deep tree: sub-batches of qc queries
+        for (int32_t q0 = 0; q0 < nq; q0 += qc) {
+            cudaError_t es = fti_launch_qt(ds, L, d_qblock + (size_t)q0 * L.stride, std::min<int32_t>(qc, nq - q0), d_docs,
+                                           docs_ld, n_docs, d_out + (int64_t)q0 * out_ld, out_ld, st);
+            if (es != cudaSuccess) return es;
+        }
+        return cudaSuccess;
+    }
     QtPlan P;
     cudaError_t e = qt_prepare(ds, L, d_qblock, nq, st, P);
     if (e != cudaSuccess) return e;
@@ -900,6 +928,16 @@ cudaError_t fti_launch_prefilter(ft_dataset* ds, const QueryLayout& L, const uin
     const int64_t n = ds->n;
     cudaError_t e;
     if (nq <= 0) return cudaSuccess;
+    const int qc = qt_fit_queries(ds, L);
+    if (qc <= 0) return cudaErrorInvalidConfiguration;
+    if (qc < QT_QC && nq > qc) {   // large supports on a deep tree: sub-batches of qc queries
+        for (int32_t q0 = 0; q0 < nq; q0 += qc)
+            if ((e = fti_launch_prefilter(ds, L, d_qblock + (size_t)q0 * L.stride, std::min<int32_t>(qc, nq - q0), m,
+                                          d_cand + (int64_t)q0 * m, d_cval + (int64_t)q0 * m, d_sel_scratch, st)) !=
+                cudaSuccess)
+                return e;
+        return cudaSuccess;
+    }
     const int64_t ns = n / 32;
     if (n < 32 * m || fti_opt(FT_OPT_PREFILTER_UNFUSED) || ns < 1) {
         if ((e = ds->s_vals.reserve(sizeof(double) * nq * n)) != cudaSuccess) return e;

@@ -614,6 +614,40 @@ def test_prefilter_overflow_fallback_in_a_chunk_pair(ft):
     assert set(got[35].tolist()) == set(range(m))
 
 
+def test_quadtree_large_supports_on_a_deep_tree_run_in_subbatches(ft):
+    """32 queries with 150-255-point supports on a deep tree (d = 3, N = 20,000 uniform points:
+    D* ~ 15, ~30k nodes) have a worst-case node union beyond the shared-memory hash of one chunk;
+    such batches are scored in sub-batches of fewer queries per chunk (40 queries: ten sub-batches
+    of 4, found by a randomised sweep — the call used to fail with a launch error).  Quadtree
+    values bit-exact on sampled pairs, and the fused prefilter + Flowtree k-NN of sampled queries
+    against the oracle pipeline."""
+    from paper_1910_04126_b200 import workloads
+    from __graft_entry__ import _ids_exact_up_to_ties
+    rng = np.random.default_rng(93)
+    N, n, nq = 20000, 2000, 40
+    X = rng.uniform(-1.0, 1.0, size=(N, 3)).astype(np.float32)
+    sampler = workloads._uniform_sampler(N)
+    doc_off, ids = workloads.sets_without_replacement(rng, rng.integers(20, 256, size=n), sampler)
+    q_off, q_ids = workloads.sets_without_replacement(rng, rng.integers(150, 256, size=nq), sampler)
+    wl = workloads.Workload("deep", X, doc_off, ids, rng.integers(1, 8, size=len(ids)).astype(np.uint32), q_off,
+                            q_ids, rng.integers(1, 8, size=len(q_ids)).astype(np.uint32), 10, 50, 32, 9093)
+    T = oracle_tree(wl)
+    ix, ds = _setup(ft, wl)
+    _, _, d_star, M = ft.ft_index_info(ix.h)
+    assert min(32 * min(255 * d_star, M), M) * 5 // 4 > 16384, "case no longer needs sub-batches"
+    qt = ds.quadtree(wl.q_off, wl.q_ids, wl.q_w)
+    pairs = [(int(q), int(d_)) for q, d_ in zip(rng.integers(0, nq, 300), rng.integers(0, n, 300))]
+    pairs += [(q, 0) for q in range(nq)]                       # every sub-batch, ragged tail included
+    ref = _oracle_all(T, wl, "qt", pairs)
+    for (q, d_), r in zip(pairs, ref):
+        assert qt[q, d_] == r[1], (q, d_)
+    gids, gvals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, wl.k, wl.prefilter_m)
+    for q in (0, 3, 4, 37, 39):
+        b, bw = wl.query(q)
+        ref_ids, ref_val = T.knn(wl.doc_off, wl.ids, wl.w, b, bw, wl.k, wl.prefilter_m)
+        _ids_exact_up_to_ties(T, wl, b, bw, gids[q], gvals[q], ref_ids, ref_val)
+
+
 def test_knn_padding_and_errors(ft):
     wl = get_workload("tiny", n_docs=7)
     ix, ds = _setup(ft, wl)
@@ -937,6 +971,22 @@ def test_topk_threshold_tie_blocks(ft):
         o = np.lexsort((np.arange(L), vals[r]))[:k]
         assert np.array_equal(oi[r], o), r
         assert np.array_equal(ov[r], vals[r][o])
+
+
+def test_randomised_parity_sweep(ft):
+    """tools/fuzz_parity.py in a fresh process: seeded random small configurations (d 1..301, N 2..5000,
+    supports 1..255, unit / small / heavy weights, duplicated points, depth caps, 1..100 queries, k,
+    prefilter m) against the oracle — paths and Quadtree values bit-exact, Flowtree within 1e-5, k-NN
+    ids up to the tie band, overflow reported by both sides — with device memory poisoned between
+    cases so that reads past an array's end see garbage.  The second range is the sequence that
+    exposed k_ftd's uniform-weight merge running past the last doc's records (seed 6862)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for args in (["--seed0", "0", "--max-cases", "400"], ["--seed0", "6855", "--max-cases", "8"]):
+        p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "--poison", "--seconds", "150"] + args,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0 and ", 0 failed" in p.stdout, (args, p.stdout[-3000:], p.stderr[-3000:])
 
 
 def test_bounds_checked_build_runs_clean(ft):

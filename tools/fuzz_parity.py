@@ -1,0 +1,173 @@
+"""Randomised parity sweep on the GPU box: many small seeded configurations (dimension, ground-set
+size, support sizes, weights, duplicated points, depth caps, batch sizes, k, prefilter m), each
+checked against the CPU oracle — node paths and Quadtree values bit-exact, Flowtree values within
+1e-5 (oracle 0 ⇒ exactly 0), k-NN ids rank by rank up to the tie band.  Test infrastructure (it
+calls oracle/); prints one line per case and a summary, exits non-zero if any case mismatched.
+
+    python tools/fuzz_parity.py [--seconds 600] [--seed0 0]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_1910_04126_b200 import flowtree as ft, workloads  # noqa: E402
+from __graft_entry__ import _ids_exact_up_to_ties  # noqa: E402
+
+FT_TOL = 1e-5
+DIMS = [1, 2, 3, 8, 16, 31, 32, 33, 40, 64, 65, 100, 128, 300, 301]
+
+
+def make_case(seed):
+    rng = np.random.default_rng(1_000_003 * seed + 17)
+    d = int(rng.choice(DIMS))
+    N = int(rng.choice([2, 3, 17, 100, 784, 1000, 5000]))
+    n = int(rng.choice([1, 2, 33, 257, 1000, 3000]))
+    nq = int(rng.choice([1, 2, 31, 33, 65, 100]))
+    kind = rng.integers(0, 3)
+    if kind == 0:
+        X = workloads.mixture_points(rng, N, d, n_comp=int(rng.integers(1, 9)))
+    elif kind == 1:
+        X = rng.uniform(-1.0, 1.0, size=(N, d)).astype(np.float32)
+    else:
+        X = rng.integers(0, 28, size=(N, d)).astype(np.float32)   # grid points, many coincide for small d
+    if N >= 4 and rng.random() < 0.3:                              # exact duplicates under distinct ids
+        src = rng.integers(0, N, size=max(1, N // 10))
+        dst = rng.integers(0, N, size=len(src))
+        X[dst] = X[src]
+    s_hi = int(min(N, rng.choice([1, 2, 5, 40, 90, 150, 255])))
+    s_lo = int(rng.integers(1, s_hi + 1))
+    zipf = rng.random() < 0.5 and s_hi * 20 <= N      # rejection sampling: Zipf sets must stay far below N
+    sampler = workloads._zipf_sampler(workloads.zipf_cdf(N)) if zipf else workloads._uniform_sampler(N)
+
+    def sets(count):
+        sizes = rng.integers(s_lo, s_hi + 1, size=count)
+        off, ids = workloads.sets_without_replacement(rng, sizes, sampler)
+        wk = rng.integers(0, 3)
+        if wk == 0:
+            w = np.ones(len(ids), np.uint32)
+        elif wk == 1:
+            w = rng.integers(1, 8, size=len(ids)).astype(np.uint32)
+        else:
+            cap = int(rng.choice([255, 4000, 65535]))              # total mass per distribution <= cap
+            w = rng.integers(1, max(1, cap // max(1, s_hi)) + 1, size=len(ids)).astype(np.uint32)
+        return off, ids, w
+
+    doc_off, ids, w = sets(n)
+    q_off, q_ids, q_w = sets(nq)
+    k = int(min(n, rng.choice([1, 3, 10, 20])))
+    m = int(rng.choice([0, k, min(n, 2 * k + 5), min(n, 100), n]))
+    if m and m < k:
+        m = k
+    depth = int(rng.choice([1, 2, 4, 8, 32, 32, 32]))
+    return workloads.Workload(f"fuzz{seed}", X, doc_off, ids, w, q_off, q_ids, q_w, k, m, depth, 7000 + seed)
+
+
+def check_case(wl, rng):
+    T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
+    assert np.array_equal(ix.paths(), T.paths), "node paths"
+    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    try:
+        qt = np.asarray(ds.quadtree(wl.q_off, wl.q_ids, wl.q_w))
+    except ft.FlowtreeError as e:
+        if "FT_EOVERFLOW" not in str(e):
+            raise
+        # a Quadtree numerator >= 2^53 (heavy masses on a deep tree) fails the whole call: the oracle
+        # must report the same overflow for at least one pair of the batch
+        pairs = [(q, dd) for q in range(wl.nq) for dd in range(wl.n)]
+        if len(pairs) > 5000:
+            pairs = [pairs[i] for i in rng.choice(len(pairs), size=5000, replace=False)]
+        for q, dd in pairs:
+            try:
+                T.qt(*wl.doc(dd), *wl.query(q))
+            except oracle.OracleError as oe:
+                assert oe.code == 3, f"oracle error {oe.code}"
+                ds.close()
+                ix.close()
+                return "both overflow"
+        raise AssertionError("GPU reports FT_EOVERFLOW, the oracle does not on the sampled pairs")
+    fl = np.asarray(ds.flowtree(wl.q_off, wl.q_ids, wl.q_w))
+    npairs = min(200, wl.nq * wl.n)
+    pq = rng.integers(0, wl.nq, size=npairs)
+    pd = rng.integers(0, wl.n, size=npairs)
+    for q, dd in zip(pq, pd):
+        b, bw = wl.query(int(q))
+        a, aw = wl.doc(int(dd))
+        ref_qt = T.qt(a, aw, b, bw)[1]
+        assert qt[q, dd] == ref_qt, f"Quadtree ({q},{dd}): {qt[q, dd]!r} vs {ref_qt!r}"
+        ref = T.ft(a, aw, b, bw)
+        g = float(fl[q, dd])
+        if ref == 0.0:
+            assert g == 0.0, f"Flowtree ({q},{dd}): oracle 0, gpu {g!r}"
+        else:
+            assert abs(g - ref) <= FT_TOL * abs(ref), f"Flowtree ({q},{dd}): {g!r} vs {ref!r}"
+    ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, wl.k, wl.prefilter_m)
+    ids, vals = np.asarray(ids), np.asarray(vals)
+    for q in rng.choice(wl.nq, size=min(4, wl.nq), replace=False):
+        b, bw = wl.query(int(q))
+        ref_ids, ref_val = T.knn(wl.doc_off, wl.ids, wl.w, b, bw, wl.k, wl.prefilter_m)
+        _ids_exact_up_to_ties(T, wl, b, bw, ids[q], vals[q], ref_ids, ref_val)
+    ds.close()
+    ix.close()
+    return "ok"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=600.0)
+    ap.add_argument("--seed0", type=int, default=0)
+    ap.add_argument("--max-cases", type=int, default=100000)
+    ap.add_argument("--poison", action="store_true",
+                    help="before each case fill and release 1 GiB of device memory with a non-zero pattern, so "
+                         "a kernel that reads scratch it never wrote sees garbage instead of a fresh process's zeros")
+    ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (e.g. FT_OPT_WARP_ONLY=1)")
+    ap.add_argument("--only", type=int, default=None, help="run this one seed (to reproduce a failure)")
+    a = ap.parse_args()
+    import torch
+    assert torch.cuda.is_available(), "fuzz_parity needs a GPU"
+    for o in a.opt:
+        name, val = o.split("=")
+        ft.ft_set_option(getattr(ft, name), int(val))
+    t0 = time.time()
+    done = 0
+    fails = 0
+    seed = a.seed0
+    if a.only is not None:
+        seed, a.max_cases = a.only, 1
+    while time.time() - t0 < a.seconds and done < a.max_cases:
+        wl = make_case(seed)
+        if a.poison:
+            pat = [-1, 0x7F7F7F7F, 0x00FFFF00, 12345678][seed % 4]
+            for _ in range(2):
+                t = torch.full((128 << 20,), pat, dtype=torch.int32, device="cuda")
+                torch.cuda.synchronize()
+                del t
+                torch.cuda.empty_cache()
+        desc = (f"seed {seed}: d={wl.X.shape[1]} N={wl.X.shape[0]} n={wl.n} nq={wl.nq} nnz={len(wl.ids)} "
+                f"k={wl.k} m={wl.prefilter_m} D={wl.max_depth} wmax={int(wl.w.max())}")
+        try:
+            res = check_case(wl, np.random.default_rng(seed))
+        except Exception as e:  # noqa: BLE001
+            print(f"FAIL {desc}: {type(e).__name__}: {e}", flush=True)
+            fails += 1
+            if fails >= 10 or "CUDA" in str(e).upper():
+                raise SystemExit(1)
+            seed += 1
+            continue
+        print(f"ok   {desc}" + ("" if res == "ok" else f"  [{res}]"), flush=True)
+        done += 1
+        seed += 1
+    print(f"fuzz_parity: {done} cases ok, {fails} failed in {time.time() - t0:.0f} s (seeds {a.seed0}..{seed - 1})")
+    if fails:
+        raise SystemExit(1)
+
+
+if __name__ == "__main__":
+    main()
