@@ -12,6 +12,7 @@ import sys
 import time
 
 import numpy as np
+import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -24,12 +25,15 @@ FT_TOL = 1e-5
 DIMS = [1, 2, 3, 8, 16, 31, 32, 33, 40, 64, 65, 100, 128, 300, 301]
 
 
-def make_case(seed):
+def make_case(seed, gen=2):
+    """gen 1: the first sweep's size lists (kept so that its seeds reproduce); gen 2 adds larger
+    ground sets, doc counts, batches and supports beyond the lane-per-pair kernel's 254."""
     rng = np.random.default_rng(1_000_003 * seed + 17)
+    big = gen >= 2
     d = int(rng.choice(DIMS))
-    N = int(rng.choice([2, 3, 17, 100, 784, 1000, 5000]))
-    n = int(rng.choice([1, 2, 33, 257, 1000, 3000]))
-    nq = int(rng.choice([1, 2, 31, 33, 65, 100]))
+    N = int(rng.choice([2, 3, 17, 100, 784, 1000, 5000] + ([40000] if big else [])))
+    n = int(rng.choice([1, 2, 33, 257, 1000, 3000] + ([20000] if big else [])))
+    nq = int(rng.choice([1, 2, 31, 33, 65, 100] + ([300] if big else [])))
     kind = rng.integers(0, 3)
     if kind == 0:
         X = workloads.mixture_points(rng, N, d, n_comp=int(rng.integers(1, 9)))
@@ -41,7 +45,7 @@ def make_case(seed):
         src = rng.integers(0, N, size=max(1, N // 10))
         dst = rng.integers(0, N, size=len(src))
         X[dst] = X[src]
-    s_hi = int(min(N, rng.choice([1, 2, 5, 40, 90, 150, 255])))
+    s_hi = int(min(N, rng.choice([1, 2, 5, 40, 90, 150, 255] + ([254, 400] if big else []))))
     s_lo = int(rng.integers(1, s_hi + 1))
     zipf = rng.random() < 0.5 and s_hi * 20 <= N      # rejection sampling: Zipf sets must stay far below N
     sampler = workloads._zipf_sampler(workloads.zipf_cdf(N)) if zipf else workloads._uniform_sampler(N)
@@ -73,10 +77,14 @@ def check_case(wl, rng):
     T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
     ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
     assert np.array_equal(ix.paths(), T.paths), "node paths"
-    ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
+    smax = int(max(np.diff(wl.doc_off).max(), np.diff(wl.q_off).max()))
     try:
+        ds = ft.Dataset(ix, wl.doc_off, wl.ids, wl.w)
         qt = np.asarray(ds.quadtree(wl.q_off, wl.q_ids, wl.q_w))
     except ft.FlowtreeError as e:
+        if "FT_ERANGE" in str(e) and smax * max(1, ix.d_star) > 8192:
+            ix.close()
+            return "support x depth > 8192 rejected"      # the documented size limit (flowtree.h)
         if "FT_EOVERFLOW" not in str(e):
             raise
         # a Quadtree numerator >= 2^53 (heavy masses on a deep tree) fails the whole call: the oracle
@@ -108,6 +116,32 @@ def check_case(wl, rng):
             assert g == 0.0, f"Flowtree ({q},{dd}): oracle 0, gpu {g!r}"
         else:
             assert abs(g - ref) <= FT_TOL * abs(ref), f"Flowtree ({q},{dd}): {g!r} vs {ref!r}"
+    # flows of a few pairs, triple by triple in canonical order (the warp kernel's export)
+    for q, dd in list(zip(pq, pd))[:3]:
+        b, bw = wl.query(int(q))
+        g = ds.flow(b, bw, int(dd))
+        o = T.flow(*wl.doc(int(dd)), b, bw)
+        for key in ("src", "dst", "mass", "node"):
+            assert np.array_equal(g[key], o[key].astype(g[key].dtype)), f"flow ({q},{dd}) {key}"
+    # a doc subset with repeats (one list for the batch) and per-query candidate lists with -1 padding
+    sub = rng.integers(0, wl.n, size=int(rng.integers(1, 70))).astype(np.int64)
+    qs = np.asarray(ds.quadtree(wl.q_off, wl.q_ids, wl.q_w, docs=sub))
+    fs = np.asarray(ds.flowtree(wl.q_off, wl.q_ids, wl.q_w, docs=sub))
+    assert np.array_equal(qs, qt[:, sub]), "Quadtree over a doc subset differs from the all-docs values"
+    np.testing.assert_allclose(fs, fl[:, sub], rtol=2e-6, atol=0, err_msg="Flowtree over a doc subset")
+    L = int(rng.integers(1, 40))
+    cand = rng.integers(-1, wl.n, size=(wl.nq, L)).astype(np.int64)
+    dev = torch.device("cuda:0")
+    out = torch.empty(cand.shape, dtype=torch.float64, device=dev)
+    ft.ft_flowtree_estimate_lists(ds.h, wl.q_off, torch.from_numpy(wl.q_ids).to(dev),
+                                  torch.from_numpy(wl.q_w.view(np.int32)).to(dev).view(torch.uint32),
+                                  torch.from_numpy(cand).to(dev), out)
+    ds.synchronize(torch.cuda.current_stream())
+    o = out.cpu().numpy()
+    pad = cand < 0
+    assert np.all(np.isinf(o[pad])), "padding candidates must score +inf"
+    ref = np.take_along_axis(fl, np.where(pad, 0, cand), 1)
+    np.testing.assert_allclose(o[~pad], ref[~pad], rtol=2e-6, atol=0, err_msg="Flowtree over candidate lists")
     ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, wl.k, wl.prefilter_m)
     ids, vals = np.asarray(ids), np.asarray(vals)
     for q in rng.choice(wl.nq, size=min(4, wl.nq), replace=False):
@@ -128,6 +162,7 @@ def main():
                     help="before each case fill and release 1 GiB of device memory with a non-zero pattern, so "
                          "a kernel that reads scratch it never wrote sees garbage instead of a fresh process's zeros")
     ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (e.g. FT_OPT_WARP_ONLY=1)")
+    ap.add_argument("--gen", type=int, default=2, help="case generator version (1: the first sweep's size lists)")
     ap.add_argument("--only", type=int, default=None, help="run this one seed (to reproduce a failure)")
     a = ap.parse_args()
     import torch
@@ -142,7 +177,7 @@ def main():
     if a.only is not None:
         seed, a.max_cases = a.only, 1
     while time.time() - t0 < a.seconds and done < a.max_cases:
-        wl = make_case(seed)
+        wl = make_case(seed, a.gen)
         if a.poison:
             pat = [-1, 0x7F7F7F7F, 0x00FFFF00, 12345678][seed % 4]
             for _ in range(2):
