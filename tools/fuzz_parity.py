@@ -142,6 +142,29 @@ def check_case(wl, rng):
     assert np.all(np.isinf(o[pad])), "padding candidates must score +inf"
     ref = np.take_along_axis(fl, np.where(pad, 0, cand), 1)
     np.testing.assert_allclose(o[~pad], ref[~pad], rtol=2e-6, atol=0, err_msg="Flowtree over candidate lists")
+    # exact W1 (transportation simplex) on small supports against the oracle's LP
+    if smax <= 40:
+        nqe = min(4, wl.nq)
+        ed = rng.integers(0, wl.n, size=(wl.nq, 3)).astype(np.int64)
+        ex = ft.ft_exact_w1_lists(ds.h, wl.q_off, wl.q_ids, wl.q_w, torch.from_numpy(ed).to(dev)).cpu().numpy()
+        for q in range(nqe):
+            b, bw = wl.query(q)
+            for jx in range(3):
+                a_, aw_ = wl.doc(int(ed[q, jx]))
+                ref_w1 = oracle.exact_w1(wl.X, a_, aw_, b, bw)
+                g = float(ex[q, jx])
+                assert abs(g - ref_w1) <= 1e-6 * ref_w1 + 1e-12 * (ref_w1 == 0.0) or (ref_w1 == 0.0 and g == 0.0), \
+                    f"exact W1 ({q},{int(ed[q, jx])}): {g!r} vs {ref_w1!r}"
+                assert g <= float(fl[q, ed[q, jx]]) * (1 + 1e-6) + 1e-12, "exact W1 above Flowtree"
+    # ft_topk on a tie-heavy random matrix against numpy's (value, id) order
+    R, Lk = int(rng.integers(1, 6)), int(rng.choice([1, 7, 300, 5000, 40000]))
+    kk = int(min(Lk, rng.choice([1, 5, 64, 1000])))
+    tv = rng.integers(0, int(rng.choice([2, 50, 100000])), size=(R, Lk)).astype(np.float64)
+    oi, ov = ft.ft_topk(torch.from_numpy(tv).to(dev), kk, id_base=5)
+    torch.cuda.synchronize()
+    for r in range(R):
+        o_ = np.lexsort((np.arange(Lk), tv[r]))[:kk]
+        assert np.array_equal(oi[r].cpu().numpy(), 5 + o_) and np.array_equal(ov[r].cpu().numpy(), tv[r][o_]), "ft_topk"
     ids, vals = ds.knn(wl.q_off, wl.q_ids, wl.q_w, wl.k, wl.prefilter_m)
     ids, vals = np.asarray(ids), np.asarray(vals)
     for q in rng.choice(wl.nq, size=min(4, wl.nq), replace=False):

@@ -1,3 +1,3 @@
 set -u
 mkdir -p gpurun_out
-timeout 1300 python tools/fuzz_parity.py --poison --seconds 1000 > gpurun_out/fuzz2.log 2>&1; echo "fuzz rc $?" >> gpurun_out/fuzz2.log
+timeout 900 python tools/fuzz_parity.py --poison --seconds 600 --seed0 2000 > gpurun_out/fuzz3.log 2>&1; echo "fuzz rc $?" >> gpurun_out/fuzz3.log
