@@ -983,7 +983,10 @@ def test_randomised_parity_sweep(ft):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for args in (["--seed0", "0", "--max-cases", "300"], ["--gen", "1", "--seed0", "6855", "--max-cases", "8"]):
+    # --directed: the documented size limits (2048-point supports at support x depth = 8192, 1000-point
+    # supports through the distance table, N beyond the vocab bitmap, k = prefilter_m = 8192)
+    for args in (["--seed0", "0", "--max-cases", "300"], ["--gen", "1", "--seed0", "6855", "--max-cases", "8"],
+                 ["--directed"]):
         p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "--poison", "--seconds", "150"] + args,
                            capture_output=True, text=True, timeout=600)
         assert p.returncode == 0 and ", 0 failed" in p.stdout, (args, p.stdout[-3000:], p.stderr[-3000:])

@@ -73,6 +73,31 @@ def make_case(seed, gen=2):
     return workloads.Workload(f"fuzz{seed}", X, doc_off, ids, w, q_off, q_ids, q_w, k, m, depth, 7000 + seed)
 
 
+def make_custom(seed, d, N, n, nq, s_lo, s_hi, depth, k, m, kind="uniform"):
+    """A directed case at the documented limits (see DIRECTED)."""
+    rng = np.random.default_rng(77_000 + seed)
+    X = (workloads.mixture_points(rng, N, d) if kind == "mixture"
+         else rng.uniform(-1.0, 1.0, size=(N, d)).astype(np.float32))
+    sampler = workloads._uniform_sampler(N)
+    doc_off, ids = workloads.sets_without_replacement(rng, rng.integers(s_lo, s_hi + 1, size=n), sampler)
+    q_off, q_ids = workloads.sets_without_replacement(rng, rng.integers(s_lo, s_hi + 1, size=nq), sampler)
+    return workloads.Workload(f"directed{seed}", X, doc_off, ids, np.ones(len(ids), np.uint32), q_off, q_ids,
+                              np.ones(len(q_ids), np.uint32), k, m, depth, 8000 + seed)
+
+
+# the size limits include/flowtree.h documents: support 2048 (support x depth <= 8192), supports of
+# 1000 through the distance table (11 column groups per query), N beyond the 2^19-id vocab bitmap
+# (hash lookups; with and without a table), k = prefilter_m = 8192
+DIRECTED = [
+    dict(d=8, N=50000, n=40, nq=3, s_lo=1500, s_hi=2048, depth=4, k=5, m=0),
+    dict(d=300, N=5000, n=60, nq=3, s_lo=700, s_hi=1000, depth=32, k=5, m=0, kind="mixture"),
+    dict(d=4, N=600000, n=2000, nq=10, s_lo=5, s_hi=20, depth=32, k=10, m=100),
+    dict(d=40, N=600000, n=500, nq=5, s_lo=5, s_hi=30, depth=32, k=10, m=0, kind="mixture"),
+    dict(d=16, N=3000, n=9000, nq=2, s_lo=1, s_hi=4, depth=32, k=8192, m=8192),
+    dict(d=300, N=2000, n=300, nq=70, s_lo=200, s_hi=254, depth=32, k=10, m=0, kind="mixture"),
+]
+
+
 def check_case(wl, rng):
     T = oracle.Tree(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
     ix = ft.Index(wl.X, seed=wl.tree_seed, max_depth=wl.max_depth)
@@ -90,8 +115,8 @@ def check_case(wl, rng):
         # a Quadtree numerator >= 2^53 (heavy masses on a deep tree) fails the whole call: the oracle
         # must report the same overflow for at least one pair of the batch
         pairs = [(q, dd) for q in range(wl.nq) for dd in range(wl.n)]
-        if len(pairs) > 5000:
-            pairs = [pairs[i] for i in rng.choice(len(pairs), size=5000, replace=False)]
+        if len(pairs) > 400000:     # (seed 20313 of the second sweep: exactly 1 of 100,000 pairs overflows)
+            pairs = [pairs[i] for i in rng.choice(len(pairs), size=400000, replace=False)]
         for q, dd in pairs:
             try:
                 T.qt(*wl.doc(dd), *wl.query(q))
@@ -185,6 +210,7 @@ def main():
                     help="before each case fill and release 1 GiB of device memory with a non-zero pattern, so "
                          "a kernel that reads scratch it never wrote sees garbage instead of a fresh process's zeros")
     ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (e.g. FT_OPT_WARP_ONLY=1)")
+    ap.add_argument("--directed", action="store_true", help="run the DIRECTED limit cases instead of the random sweep")
     ap.add_argument("--gen", type=int, default=2, help="case generator version (1: the first sweep's size lists)")
     ap.add_argument("--only", type=int, default=None, help="run this one seed (to reproduce a failure)")
     a = ap.parse_args()
@@ -199,8 +225,10 @@ def main():
     seed = a.seed0
     if a.only is not None:
         seed, a.max_cases = a.only, 1
-    while time.time() - t0 < a.seconds and done < a.max_cases:
-        wl = make_case(seed, a.gen)
+    if a.directed:
+        a.max_cases, seed, a.seconds = len(DIRECTED), 0, 1e9
+    while time.time() - t0 < a.seconds and done + fails < a.max_cases:
+        wl = make_custom(seed, **DIRECTED[seed]) if a.directed else make_case(seed, a.gen)
         if a.poison:
             pat = [-1, 0x7F7F7F7F, 0x00FFFF00, 12345678][seed % 4]
             for _ in range(2):
