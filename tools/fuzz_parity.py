@@ -210,6 +210,10 @@ def main():
                     help="before each case fill and release 1 GiB of device memory with a non-zero pattern, so "
                          "a kernel that reads scratch it never wrote sees garbage instead of a fresh process's zeros")
     ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (e.g. FT_OPT_WARP_ONLY=1)")
+    ap.add_argument("--random-opts", action="store_true",
+                    help="per case, switch a random subset of the library's alternative code paths on (hash lookups, "
+                         "warp kernel only, radix selection, unfused prefilter, single-chunk Quadtree scan, query-major "
+                         "tables, small table chunks): every path must agree with the oracle")
     ap.add_argument("--directed", action="store_true", help="run the DIRECTED limit cases instead of the random sweep")
     ap.add_argument("--gen", type=int, default=2, help="case generator version (1: the first sweep's size lists)")
     ap.add_argument("--only", type=int, default=None, help="run this one seed (to reproduce a failure)")
@@ -229,6 +233,18 @@ def main():
         a.max_cases, seed, a.seconds = len(DIRECTED), 0, 1e9
     while time.time() - t0 < a.seconds and done + fails < a.max_cases:
         wl = make_custom(seed, **DIRECTED[seed]) if a.directed else make_case(seed, a.gen)
+        optdesc = ""
+        if a.random_opts:
+            orng = np.random.default_rng(555 + seed)
+            for o in range(ft.FT_NUM_OPTIONS):
+                ft.ft_set_option(o, 0)
+            for name, val in (("FT_OPT_VOCAB_HASH", 1), ("FT_OPT_WARP_ONLY", 1), ("FT_OPT_QT_HASH", 1),
+                              ("FT_OPT_SELECT_RADIX", 1), ("FT_OPT_PREFILTER_UNFUSED", 1), ("FT_OPT_QT_PAIR_OFF", 1),
+                              ("FT_OPT_DIST_QMAJOR", 1), ("FT_OPT_TABLE_CHUNK", int(orng.integers(1, 40))),
+                              ("FT_OPT_EXACT_START_NW", 1), ("FT_OPT_QT_WAVES", int(orng.integers(1, 17)))):
+                if orng.random() < 0.3:
+                    ft.ft_set_option(getattr(ft, name), val)
+                    optdesc += f" {name[7:]}={val}"
         if a.poison:
             pat = [-1, 0x7F7F7F7F, 0x00FFFF00, 12345678][seed % 4]
             for _ in range(2):
@@ -237,7 +253,7 @@ def main():
                 del t
                 torch.cuda.empty_cache()
         desc = (f"seed {seed}: d={wl.X.shape[1]} N={wl.X.shape[0]} n={wl.n} nq={wl.nq} nnz={len(wl.ids)} "
-                f"k={wl.k} m={wl.prefilter_m} D={wl.max_depth} wmax={int(wl.w.max())}")
+                f"k={wl.k} m={wl.prefilter_m} D={wl.max_depth} wmax={int(wl.w.max())}{optdesc}")
         try:
             res = check_case(wl, np.random.default_rng(seed))
         except Exception as e:  # noqa: BLE001
