@@ -226,8 +226,18 @@ def exact_w1(X, mu_ids, mu_w, nu_ids, nu_w) -> float:
         A_eq[i, i * q:(i + 1) * q] = 1.0
     for j in range(q):
         A_eq[p + j, j::q] = 1.0
-    res = linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([a, b]), bounds=(0, None), method="highs",
-                  options={"primal_feasibility_tolerance": 1e-10, "dual_feasibility_tolerance": 1e-10})
+    # Costs and plans are non-negative and the marginals are consistent (Σa = Σb = W·U), so the LP is
+    # feasible and bounded.  With the tight tolerances HiGHS' simplex occasionally reports
+    # "unbounded" on marginals of ~1e8 (a 19 x 19 image-like pair found by the randomised sweep):
+    # the SAME LP is then re-solved with the solver's default tolerances, then by its
+    # interior-point method — a library retry, no other arithmetic.
+    res = None
+    for method, opts in (("highs", {"primal_feasibility_tolerance": 1e-10, "dual_feasibility_tolerance": 1e-10}),
+                         ("highs", {}), ("highs-ipm", {})):
+        res = linprog(C.ravel(), A_eq=A_eq, b_eq=np.concatenate([a, b]), bounds=(0, None), method=method,
+                      options=opts)
+        if res.status == 0:
+            break
     if res.status != 0:
         raise OracleError(-1, "exact_w1: " + res.message)
     return float(res.fun) / (W * U)

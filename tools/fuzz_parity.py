@@ -29,6 +29,8 @@ def make_case(seed, gen=2):
     """gen 1: the first sweep's size lists (kept so that its seeds reproduce); gen 2 adds larger
     ground sets, doc counts, batches and supports beyond the lane-per-pair kernel's 254."""
     rng = np.random.default_rng(1_000_003 * seed + 17)
+    if gen == 3:
+        return make_image_like(seed, rng)
     big = gen >= 2
     d = int(rng.choice(DIMS))
     N = int(rng.choice([2, 3, 17, 100, 784, 1000, 5000] + ([40000] if big else [])))
@@ -71,6 +73,37 @@ def make_case(seed, gen=2):
         m = k
     depth = int(rng.choice([1, 2, 4, 8, 32, 32, 32]))
     return workloads.Workload(f"fuzz{seed}", X, doc_off, ids, w, q_off, q_ids, q_w, k, m, depth, 7000 + seed)
+
+
+def make_image_like(seed, rng):
+    """gen 3: image-like cases — a small dense grid in the plane or in R^3 (every cell of the deep
+    tree is shared by many docs, so nearly every pair matches inside common multi-point cells: the
+    warp kernel's per-depth northwest corners), large supports with non-uniform integer masses."""
+    d = int(rng.choice([2, 2, 3]))
+    side = int(rng.choice([8, 16, 28]))
+    g = np.stack(np.meshgrid(*[np.arange(side)] * d, indexing="ij"), -1).reshape(-1, d).astype(np.float32)
+    if len(g) > 4096:
+        g = g[rng.choice(len(g), 4096, replace=False)]
+    N = len(g)
+    n = int(rng.choice([33, 257, 1000]))
+    nq = int(rng.choice([1, 5, 33, 70]))
+    s_hi = int(min(N, rng.choice([20, 150, 254, 300])))
+    s_lo = int(rng.integers(1, s_hi + 1))
+    sampler = workloads._uniform_sampler(N)
+
+    def sets(count):
+        off, ids = workloads.sets_without_replacement(rng, rng.integers(s_lo, s_hi + 1, size=count), sampler)
+        w = rng.integers(1, max(2, 65535 // s_hi // int(rng.choice([1, 16, 200]))), size=len(ids)).astype(np.uint32)
+        return off, ids, w
+
+    doc_off, ids, w = sets(n)
+    q_off, q_ids, q_w = sets(nq)
+    k = int(min(n, rng.choice([1, 10])))
+    m = int(rng.choice([0, min(n, 50)]))
+    if m and m < k:
+        m = k
+    depth = int(rng.choice([2, 4, 6, 8, 32]))
+    return workloads.Workload(f"img{seed}", g, doc_off, ids, w, q_off, q_ids, q_w, k, m, depth, 9000 + seed)
 
 
 def make_custom(seed, d, N, n, nq, s_lo, s_hi, depth, k, m, kind="uniform"):

@@ -1,3 +1,3 @@
 set -u
 mkdir -p gpurun_out
-timeout 1000 python tools/fuzz_parity.py --poison --random-opts --seconds 700 --seed0 30000 > gpurun_out/fuzz5.log 2>&1; echo "fuzz rc $?" >> gpurun_out/fuzz5.log
+timeout 800 python tools/fuzz_parity.py --poison --gen 3 --seconds 500 --seed0 0 > gpurun_out/fuzz6.log 2>&1; echo "fuzz rc $?" >> gpurun_out/fuzz6.log
