@@ -1,4 +1,8 @@
+# The round's GPU job (gpurun -- bash tools/gpu_job.sh): full GPU suite, smoke, both bench arms, ncu profiles.
 set -u
 mkdir -p gpurun_out
-timeout 300 python tools/fuzz_parity.py --gen 3 --only 1818 > gpurun_out/s1818.log 2>&1; echo "rc $?" >> gpurun_out/s1818.log
-FT_LIB=$PWD/paper_1910_04126_b200/libflowtree_b200_checked.so timeout 800 python tools/fuzz_parity.py --poison --random-opts --gen 3 --seconds 420 --seed0 5000 > gpurun_out/fuzz7.log 2>&1; echo "fuzz rc $?" >> gpurun_out/fuzz7.log
+timeout 1500 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_line.json 2> gpurun_out/bench_err.log; echo "bench rc $?" >> gpurun_out/bench_err.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref_err.log; echo "ref rc $?" >> gpurun_out/bench_ref_err.log
+bash tools/profile_round.sh > gpurun_out/profile_round.log 2>&1
