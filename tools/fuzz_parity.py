@@ -31,6 +31,20 @@ def make_case(seed, gen=2):
     rng = np.random.default_rng(1_000_003 * seed + 17)
     if gen == 3:
         return make_image_like(seed, rng)
+    if gen == 4:
+        # paper-shaped medium cases: d = 300 mixtures, Zipf ids, odd doc counts and batch sizes
+        # (ragged tiles, odd chunk pairs, several table chunks), prefiltered or exhaustive
+        N = int(rng.choice([5000, 50000]))
+        n = int(rng.choice([4999, 20001, 50000]))
+        nq = int(rng.choice([63, 100, 257, 500]))
+        s_lo, s_hi = [(10, 90), (10, 150), (1, 40)][int(rng.integers(0, 3))]
+        X = workloads.mixture_points(rng, N, int(rng.choice([300, 128, 65])))
+        sampler = workloads._zipf_sampler(workloads.zipf_cdf(N))
+        doc_off, ids = workloads.sets_without_replacement(rng, rng.integers(s_lo, s_hi + 1, size=n), sampler)
+        q_off, q_ids = workloads.sets_without_replacement(rng, rng.integers(s_lo, s_hi + 1, size=nq), sampler)
+        m = int(rng.choice([100, 1000, 2000] + ([0] if n < 5000 else [])))
+        return workloads.Workload(f"paper{seed}", X, doc_off, ids, np.ones(len(ids), np.uint32), q_off, q_ids,
+                                  np.ones(len(q_ids), np.uint32), 10, m, 32, 6000 + seed)
     big = gen >= 2
     d = int(rng.choice(DIMS))
     N = int(rng.choice([2, 3, 17, 100, 784, 1000, 5000] + ([40000] if big else [])))
