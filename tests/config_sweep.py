@@ -1,6 +1,6 @@
 """Run ft_knn (BASELINE config's k / prefilter) on every config with device-resident queries and
 report the device time per query batch, plus a sampled oracle check of the Quadtree and Flowtree
-values at full size.  python tools/config_sweep.py [names...]"""
+values at full size.  python tests/config_sweep.py [names...]"""
 import json
 import os
 import sys

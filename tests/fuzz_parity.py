@@ -2,9 +2,9 @@
 size, support sizes, weights, duplicated points, depth caps, batch sizes, k, prefilter m), each
 checked against the CPU oracle — node paths and Quadtree values bit-exact, Flowtree values within
 1e-5 (oracle 0 ⇒ exactly 0), k-NN ids rank by rank up to the tie band.  Test infrastructure (it
-calls oracle/); prints one line per case and a summary, exits non-zero if any case mismatched.
+calls oracle/, so it lives under tests/); prints one line per case and a summary, exits non-zero if any case mismatched.
 
-    python tools/fuzz_parity.py [--seconds 600] [--seed0 0]
+    python tests/fuzz_parity.py [--seconds 600] [--seed0 0]
 """
 import argparse
 import os

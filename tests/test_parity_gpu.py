@@ -974,7 +974,7 @@ def test_topk_threshold_tie_blocks(ft):
 
 
 def test_randomised_parity_sweep(ft):
-    """tools/fuzz_parity.py in a fresh process: seeded random small configurations (d 1..301, N 2..5000,
+    """tests/fuzz_parity.py in a fresh process: seeded random small configurations (d 1..301, N 2..5000,
     supports 1..255, unit / small / heavy weights, duplicated points, depth caps, 1..100 queries, k,
     prefilter m) against the oracle — paths and Quadtree values bit-exact, Flowtree within 1e-5, k-NN
     ids up to the tie band, overflow reported by both sides — with device memory poisoned between
@@ -987,7 +987,7 @@ def test_randomised_parity_sweep(ft):
     # supports through the distance table, N beyond the vocab bitmap, k = prefilter_m = 8192)
     for args in (["--seed0", "0", "--max-cases", "300"], ["--gen", "1", "--seed0", "6855", "--max-cases", "8"],
                  ["--directed"]):
-        p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "--poison", "--seconds", "150"] + args,
+        p = subprocess.run([sys.executable, os.path.join(root, "tests", "fuzz_parity.py"), "--poison", "--seconds", "150"] + args,
                            capture_output=True, text=True, timeout=600)
         assert p.returncode == 0 and ", 0 failed" in p.stdout, (args, p.stdout[-3000:], p.stderr[-3000:])
 
